@@ -1,0 +1,219 @@
+/*
+ * dcpx.h — C ABI of the B200-native DCP executor.
+ *
+ * This is the drop-in boundary for the executor half of DCP (arXiv 2510.10620).
+ * The reference executes per-device ExecutionPlans with the single-threaded CPU
+ * simulator `dcp::run(plans, g, payload, topo, opts) -> SimResult`
+ * (reference: proj/include/dcp/simexec.hpp:207-209). This header replaces that
+ * call with: create a context, prepare it with flat POD views of the same plans
+ * (proj/include/dcp/plan.hpp:37-107) and block graph (proj/include/dcp/blocks.hpp:19-85),
+ * load packed bf16 Q/K/V, run forward, run backward.
+ *
+ * Mapping to the reference interface (each entry point cites what it replaces):
+ *   dcpx_create / dcpx_create_rank  -> construction of the per-device slot arenas in
+ *                                      run() (simexec.hpp:216-222); one process owning
+ *                                      all plan devices (like run) or one rank per GPU.
+ *   dcpx_prepare                    -> plan ingestion + the resident-slot setup of run()
+ *                                      (simexec.hpp:223-246); also what verify_plans
+ *                                      checks statically (plan.hpp:388-475).
+ *   dcpx_load_inputs                -> make_payload + resident copies (simexec.hpp:125-146,
+ *                                      223-246): packed Q/K/V scattered to resident slots.
+ *   dcpx_forward                    -> the lockstep interpreter of run() (simexec.hpp:258-395):
+ *                                      Attention (:328-344, exec_attention :33-76),
+ *                                      Reduction (:345-354, exec_reduction :80-111),
+ *                                      Copy (:355-368), CommLaunch/CommWait (:263-327),
+ *                                      deadlock / tag checks (:384-397), output assembly
+ *                                      (:403-421), SimReport accounting (:153-162).
+ *   dcpx_backward                   -> no reference. Gradients of the same
+ *                                      masked blockwise attention under the same plan.
+ *   dcpx_last_error                 -> dcp::Error::what() (types.hpp:17-45).
+ *
+ * Conventions
+ *   - No C++ types cross this boundary; all views are caller-owned and borrowed only
+ *     for the duration of the call.
+ *   - Status codes map 1:1 onto the reference's exception hierarchy (types.hpp:17-45).
+ *   - Tensors are device pointers (bf16 unless stated) in the caller's current CUDA
+ *     context for the context's device; "host" variants take host pointers.
+ *   - Packed token-major layouts: q/o/dq [T_total][H][D], k/v/dk/dv [T_total][G][D],
+ *     lse [H][T_total] (fp32, natural log). Sequences are concatenated in batch order.
+ *   - Only D = 128 is supported by the sm_100a kernels (north_star: d = 128).
+ */
+#ifndef DCPX_H_
+#define DCPX_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes: types.hpp:17-45 --------------------------------------------- */
+typedef enum {
+  DCPX_OK = 0,
+  DCPX_ERROR = 1,            /* dcp::Error */
+  DCPX_DEADLOCK = 2,         /* dcp::DeadlockError      (simexec.hpp:384-394) */
+  DCPX_TAG_MISMATCH = 3,     /* dcp::TagMismatchError   (simexec.hpp:267-273,317,396) */
+  DCPX_BUFFER_OVERFLOW = 4,  /* dcp::BufferOverflowError (plan.hpp:368-380) */
+  DCPX_INFEASIBLE = 5,       /* dcp::InfeasibleError (caller side: placement) */
+  DCPX_CUDA_ERROR = 6,       /* CUDA / NCCL runtime failure */
+  DCPX_UNSUPPORTED = 7       /* shape the sm_100a kernels do not handle (e.g. D != 128) */
+} dcpx_status;
+
+typedef enum { DCPX_TRANSPORT_LOCAL = 0, DCPX_TRANSPORT_NCCL = 1 } dcpx_transport;
+
+/* ---- block graph view: blocks.hpp:19-85 ---------------------------------------- */
+enum { DCPX_KIND_Q = 0, DCPX_KIND_KV = 1, DCPX_KIND_O = 2 }; /* BlockKind, blocks.hpp:8 */
+
+typedef struct {            /* DataBlock, blocks.hpp:19-27 */
+  int32_t id, kind, seq, head, tile, _pad;
+  int64_t tok_begin, tok_end; /* [start, end) within the sequence */
+  uint64_t size_bytes;
+} dcpx_data_block;
+
+typedef struct {            /* ComputationBlock, blocks.hpp:29-40 */
+  int32_t id, q_block, kv_block, o_block, seq, head, q_tile, kv_tile;
+  uint64_t attended_pairs, flops_weight;
+} dcpx_comp_block;
+
+typedef struct {            /* BlockGraph + Batch (types.hpp:245-274) */
+  int32_t heads, kv_groups, head_dim, bytes_per_element;
+  int32_t num_seqs, num_data_blocks, num_comp_blocks, _pad;
+  const int64_t* seq_lengths;        /* [num_seqs] */
+  const int64_t* block_sizes;        /* [num_seqs]  BlockGraph::block_sizes */
+  const dcpx_data_block* data_blocks;/* [num_data_blocks] */
+  const dcpx_comp_block* comp_blocks;/* [num_comp_blocks] */
+} dcpx_graph_view;
+
+/* Per-sequence attend ranges (AttendRanges, types.hpp:232-243 / masks.hpp:10-67),
+ * flattened: token i of sequence s is row seq_offsets[s] + i, four int32
+ * (b0, e0, b1, e1) in sequence-local coordinates; an absent range is (0, 0). */
+typedef struct {
+  const int64_t* seq_offsets; /* [num_seqs + 1] */
+  const int32_t* ranges;      /* [seq_offsets[num_seqs]][4] */
+} dcpx_mask_view;
+
+/* ---- execution plan view: plan.hpp:37-107 -------------------------------------- */
+enum {
+  DCPX_OP_ATTENTION = 0,   /* AttentionInstr  plan.hpp:50-52 */
+  DCPX_OP_REDUCTION = 1,   /* ReductionInstr  plan.hpp:54-57 */
+  DCPX_OP_COPY = 2,        /* CopyInstr       plan.hpp:59-66 */
+  DCPX_OP_COMM_LAUNCH = 3, /* CommLaunchInstr plan.hpp:73-78 */
+  DCPX_OP_COMM_WAIT = 4    /* CommWaitInstr   plan.hpp:80-82 */
+};
+
+typedef struct {           /* AttentionItem, plan.hpp:37-48 */
+  int32_t comp_id, q_slot, kv_slot, out_slot, seq, head;
+  int64_t q_begin, q_end;   /* q_tokens  */
+  int64_t kv_begin, kv_end; /* kv_tokens */
+  /* Row ranges (AttentionItem::rows, relative to kv_begin, plan.hpp:231-242).
+   * -1: derive them from the mask view (bit-identical to compile_plans);
+   * otherwise an offset into dcpx_plan_view.rows, (q_end-q_begin) rows of 4 int32. */
+  int64_t rows_offset;
+} dcpx_attention_item;
+
+typedef struct { int32_t block, slot; } dcpx_block_slot; /* TransferBlock / ResidentBlock */
+typedef struct { int32_t src_slot, dst_slot; } dcpx_copy_item; /* CopyItem */
+
+typedef struct {           /* Instruction, plan.hpp:84-87 */
+  int32_t op;              /* DCPX_OP_* */
+  int32_t division;        /* Instruction::division */
+  int32_t send;            /* CommLaunch: 1 = send, 0 = receive */
+  int32_t peer;            /* CommLaunch: peer device */
+  int32_t dst;             /* Reduction: destination slot */
+  int32_t count;           /* items / srcs / copy items / blocks */
+  int64_t offset;          /* first element in the op's pool below */
+  const char* tag;         /* CommLaunch / CommWait tag (NUL-terminated) */
+} dcpx_instruction;
+
+typedef struct {           /* ExecutionPlan, plan.hpp:101-107 */
+  int32_t version, device, divisions, _pad;
+  int32_t capacity[3];     /* BufferLayout::capacity, indexed by kind */
+  int32_t n_resident_q, n_resident_kv, n_resident_o;
+  const dcpx_block_slot* resident_q;
+  const dcpx_block_slot* resident_kv;
+  const dcpx_block_slot* resident_o;
+  int32_t n_instructions, _pad2;
+  const dcpx_instruction* instructions;
+  const dcpx_attention_item* items;  /* pool for DCPX_OP_ATTENTION */
+  const int32_t* srcs;               /* pool for DCPX_OP_REDUCTION */
+  const dcpx_copy_item* copies;      /* pool for DCPX_OP_COPY */
+  const dcpx_block_slot* blocks;     /* pool for DCPX_OP_COMM_LAUNCH */
+  const int32_t* rows;               /* optional explicit item rows, [n][4] */
+} dcpx_plan_view;
+
+/* ---- report: SimReport, simexec.hpp:153-162 ------------------------------------ */
+typedef struct {
+  int32_t devices, stages;           /* stages = divisions + 1 (stage T = output stage) */
+  uint64_t total_bytes;              /* planned bytes moved (SimReport::total_bytes) */
+  uint64_t total_flops;              /* 4 * pairs * D summed over executed items */
+  uint64_t per_device_send[64];
+  uint64_t per_device_recv[64];
+  uint64_t wire_bytes;               /* bytes actually moved incl. fp32 LSE/Delta sidecars */
+  double makespan;                   /* modeled, detail::cost_from_tables (schedule.hpp:217-236) */
+  double device_ms;                  /* measured device time of the last call (max over devices) */
+  int32_t kernel_launches;           /* executor kernels launched by the last call */
+  int32_t _pad;
+} dcpx_report;
+
+typedef struct dcpx_ctx dcpx_ctx;
+
+/* One process executes all `ndev` plan devices; plan device d runs on CUDA device
+ * cuda_ordinals[d] (several plan devices may share one GPU). Transfers are
+ * device-to-device copies on per-device comm streams. transport must be LOCAL. */
+dcpx_status dcpx_create(int ndev, const int* cuda_ordinals, dcpx_transport transport,
+                        dcpx_ctx** out);
+
+/* One plan device per process (rank == plan device), NCCL point-to-point over
+ * NVLink. nccl_unique_id points to the 128-byte ncclUniqueId created by rank 0 and
+ * broadcast by the caller (e.g. torch.distributed). */
+dcpx_status dcpx_create_rank(int rank, int world, int cuda_ordinal, const void* nccl_unique_id,
+                             dcpx_ctx** out);
+
+/* Returns the 128-byte ncclUniqueId to broadcast (rank 0 calls this). */
+dcpx_status dcpx_nccl_unique_id(void* out128);
+
+/* Ingests the plans. In LOCAL mode `plans` holds all ndev plans in device order; in
+ * NCCL mode it holds exactly this rank's plan (plans[0].device == rank). Validates
+ * shapes, slots and tag pairing, sizes the slot arenas from BufferLayout::capacity,
+ * and compiles the instruction stream into the device program. */
+dcpx_status dcpx_prepare(dcpx_ctx* ctx, int nplans, const dcpx_plan_view* plans,
+                         const dcpx_graph_view* graph, const dcpx_mask_view* masks);
+
+/* Packed bf16 inputs on the context's device(s): q [T][H][D], k, v [T][G][D].
+ * In LOCAL mode with several GPUs, pointers refer to cuda_ordinals[0]'s memory and
+ * are copied peer-to-peer to the owners. Scatters rows into the resident slots. */
+dcpx_status dcpx_load_inputs(dcpx_ctx* ctx, const void* q, const void* k, const void* v);
+/* Same with host (pinned or pageable) pointers; host->device copies are inside. */
+dcpx_status dcpx_load_inputs_host(dcpx_ctx* ctx, const void* q, const void* k, const void* v);
+
+/* Executes the plan forward. o_out [T][H][D] bf16 and lse_out [H][T] fp32 (may be
+ * NULL) receive the rows owned by this context's device(s); other rows untouched. */
+dcpx_status dcpx_forward(dcpx_ctx* ctx, void* o_out, float* lse_out, dcpx_report* rep);
+dcpx_status dcpx_forward_host(dcpx_ctx* ctx, void* o_out, float* lse_out, dcpx_report* rep);
+
+/* Executes the backward of the last forward. d_o [T][H][D] bf16 in; dq [T][H][D],
+ * dk, dv [T][G][D] bf16 out (owned rows). */
+dcpx_status dcpx_backward(dcpx_ctx* ctx, const void* d_o, void* dq, void* dk, void* dv,
+                          dcpx_report* rep);
+dcpx_status dcpx_backward_host(dcpx_ctx* ctx, const void* d_o, void* dq, void* dk, void* dv,
+                               dcpx_report* rep);
+
+/* Synchronises all streams of the context. */
+dcpx_status dcpx_synchronize(dcpx_ctx* ctx);
+
+/* Test / introspection hooks (not part of the reference surface). */
+/* Device pointers of the slot arenas of plan device `dev`: kind 0 Q, 1 KV, 2 O, 3 LSE. */
+dcpx_status dcpx_debug_arena(dcpx_ctx* ctx, int dev, int kind, void** ptr, int64_t* slot_rows);
+/* Executor options: key "fuse_reductions", "remap_copies", "check_rows", "timing". */
+dcpx_status dcpx_set_option(dcpx_ctx* ctx, const char* key, int64_t value);
+
+const char* dcpx_last_error(dcpx_ctx* ctx);
+const char* dcpx_version(void);
+void dcpx_destroy(dcpx_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* DCPX_H_ */
