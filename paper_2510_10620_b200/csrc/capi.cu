@@ -1,0 +1,130 @@
+// capi.cu — extern "C" boundary (include/dcpx.h). No exception crosses it: every
+// dcpx::Failure maps onto its dcpx_status, mirroring the reference's exception types
+// (types.hpp:17-45); the message is kept per context (dcpx_last_error).
+#include <cstring>
+#include <string>
+
+#include "executor.h"
+
+struct dcpx_ctx {
+  dcpx::Executor* ex = nullptr;
+  std::string err;
+};
+
+namespace {
+thread_local std::string g_create_err;
+
+template <class F>
+dcpx_status guarded(dcpx_ctx* ctx, F&& f) {
+  if (!ctx || !ctx->ex) return DCPX_ERROR;
+  try {
+    f(*ctx->ex);
+    return DCPX_OK;
+  } catch (const dcpx::Failure& e) {
+    ctx->err = e.what();
+    return e.code;
+  } catch (const std::exception& e) {
+    ctx->err = e.what();
+    return DCPX_ERROR;
+  }
+}
+}  // namespace
+
+extern "C" {
+
+const char* dcpx_version(void) { return "dcpx 0.1 (sm_100a tcgen05)"; }
+
+dcpx_status dcpx_create(int ndev, const int* cuda_ordinals, dcpx_transport transport, dcpx_ctx** out) {
+  if (!out) return DCPX_ERROR;
+  *out = nullptr;
+  if (transport != DCPX_TRANSPORT_LOCAL) {
+    g_create_err = "dcpx_create: only the LOCAL transport is process-local; use dcpx_create_rank for NCCL";
+    return DCPX_ERROR;
+  }
+  try {
+    auto* c = new dcpx_ctx;
+    c->ex = new dcpx::Executor(ndev, cuda_ordinals);
+    *out = c;
+    return DCPX_OK;
+  } catch (const dcpx::Failure& e) {
+    g_create_err = e.what();
+    return e.code;
+  } catch (const std::exception& e) {
+    g_create_err = e.what();
+    return DCPX_ERROR;
+  }
+}
+
+dcpx_status dcpx_prepare(dcpx_ctx* ctx, int nplans, const dcpx_plan_view* plans,
+                         const dcpx_graph_view* graph, const dcpx_mask_view* masks) {
+  return guarded(ctx, [&](dcpx::Executor& ex) { ex.prepare(nplans, plans, graph, masks); });
+}
+
+dcpx_status dcpx_load_inputs(dcpx_ctx* ctx, const void* q, const void* k, const void* v) {
+  return guarded(ctx, [&](dcpx::Executor& ex) { ex.load_inputs(q, k, v, false); });
+}
+
+dcpx_status dcpx_load_inputs_host(dcpx_ctx* ctx, const void* q, const void* k, const void* v) {
+  return guarded(ctx, [&](dcpx::Executor& ex) { ex.load_inputs(q, k, v, true); });
+}
+
+dcpx_status dcpx_forward(dcpx_ctx* ctx, void* o_out, float* lse_out, dcpx_report* rep) {
+  return guarded(ctx, [&](dcpx::Executor& ex) { ex.forward(o_out, lse_out, rep, false); });
+}
+
+dcpx_status dcpx_forward_host(dcpx_ctx* ctx, void* o_out, float* lse_out, dcpx_report* rep) {
+  return guarded(ctx, [&](dcpx::Executor& ex) { ex.forward(o_out, lse_out, rep, true); });
+}
+
+dcpx_status dcpx_synchronize(dcpx_ctx* ctx) {
+  return guarded(ctx, [&](dcpx::Executor& ex) { ex.synchronize(); });
+}
+
+dcpx_status dcpx_debug_arena(dcpx_ctx* ctx, int dev, int kind, void** ptr, int64_t* slot_rows) {
+  return guarded(ctx, [&](dcpx::Executor& ex) { ex.debug_arena(dev, kind, ptr, slot_rows); });
+}
+
+dcpx_status dcpx_set_option(dcpx_ctx* ctx, const char* key, int64_t value) {
+  return guarded(ctx, [&](dcpx::Executor& ex) {
+    const std::string k = key ? key : "";
+    if (k == "fuse_reductions") ex.opt.fuse_reductions = value != 0;
+    else if (k == "remap_copies") ex.opt.remap_copies = value != 0;
+    else if (k == "check_rows") ex.opt.check_rows = value != 0;
+    else if (k == "timing") ex.opt.timing = value != 0;
+    else throw dcpx::Failure(DCPX_ERROR, "unknown option " + k);
+  });
+}
+
+const char* dcpx_last_error(dcpx_ctx* ctx) {
+  if (!ctx) return g_create_err.c_str();
+  return ctx->err.c_str();
+}
+
+void dcpx_destroy(dcpx_ctx* ctx) {
+  if (!ctx) return;
+  try {
+    delete ctx->ex;
+  } catch (...) {
+  }
+  delete ctx;
+}
+
+}  // extern "C"
+
+// ---- entry points implemented in later milestones (backward, NCCL transport) -----------
+extern "C" {
+dcpx_status dcpx_create_rank(int, int, int, const void*, dcpx_ctx** out) {
+  if (out) *out = nullptr;
+  g_create_err = "dcpx_create_rank: NCCL transport not built yet";
+  return DCPX_UNSUPPORTED;
+}
+dcpx_status dcpx_nccl_unique_id(void*) { return DCPX_UNSUPPORTED; }
+dcpx_status dcpx_backward(dcpx_ctx* ctx, const void*, void*, void*, void*, dcpx_report*) {
+  if (ctx) ctx->err = "backward not built yet";
+  return DCPX_UNSUPPORTED;
+}
+dcpx_status dcpx_backward_host(dcpx_ctx* ctx, const void*, void*, void*, void*, dcpx_report*) {
+  if (ctx) ctx->err = "backward not built yet";
+  return DCPX_UNSUPPORTED;
+}
+}

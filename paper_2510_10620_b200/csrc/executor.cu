@@ -1,0 +1,1080 @@
+// executor.cu — host side of the B200 DCP executor.
+//
+// Replaces dcp::run (simexec.hpp:207-423). prepare() ingests the per-device plans
+// (plan.hpp:101-107) and the block graph, re-checks them statically the way
+// verify_plans does (plan.hpp:388-475), replays the reference's lockstep interpreter
+// symbolically (simexec.hpp:375-397) to detect deadlocks / tag mismatches and to fix
+// a global issue order, and compiles each device's instruction stream into a device
+// program:
+//   AttentionInstr (+ the ReductionInstrs that merge its partials)  -> one fused
+//       attn_fwd launch (FwdUnit/FwdStep lists, masks classified per 128x128 tile)
+//   remaining ReductionInstrs                                        -> merge launch
+//   CopyInstr                                                        -> slot remap (or
+//       a copy launch when the source is touched again)
+//   CommLaunch / CommWait                                            -> event-ordered
+//       transfers on a per-device comm stream (LOCAL transport: one copy kernel per
+//       message reading the sender's arena, peer-to-peer across GPUs).
+// forward() then issues the programs in the recorded order; no host sync inside.
+#include <cuda_bf16.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <array>
+#include <cmath>
+#include <cstring>
+#include <numeric>
+#include <set>
+
+#include "executor.h"
+
+namespace dcpx {
+
+#define CUDA_OK(x)                                                                        \
+  do {                                                                                    \
+    cudaError_t e__ = (x);                                                                \
+    if (e__ != cudaSuccess)                                                               \
+      throw Failure(DCPX_CUDA_ERROR, std::string(#x) + ": " + cudaGetErrorString(e__));   \
+  } while (0)
+
+namespace {
+
+struct DeviceGuard {
+  int prev = 0;
+  explicit DeviceGuard(int d) {
+    cudaGetDevice(&prev);
+    cudaSetDevice(d);
+  }
+  ~DeviceGuard() { cudaSetDevice(prev); }
+};
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    CUDA_OK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+    if (!p) throw Failure(DCPX_CUDA_ERROR, "cuTensorMapEncodeTiled unavailable");
+    fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+// 2-D bf16 tensor map over an arena of `rows` x 128, box 128 rows x 64 columns,
+// 128-byte swizzle (matches the UMMA SWIZZLE_128B descriptors in sm100.cuh).
+CUtensorMap make_tmap(void* base, int64_t rows) {
+  CUtensorMap m;
+  cuuint64_t dims[2] = {128, static_cast<cuuint64_t>(rows)};
+  cuuint64_t strides[1] = {256};
+  cuuint32_t box[2] = {64, 128};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, base, dims, strides, box, es,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw Failure(DCPX_CUDA_ERROR, "cuTensorMapEncodeTiled failed: " + std::to_string(r));
+  return m;
+}
+
+int num_sms(int ordinal) {
+  int n = 0;
+  cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, ordinal);
+  return n > 0 ? n : 148;
+}
+
+struct RelRange {
+  int32_t b0, e0, b1, e1;  // kv-tile-relative, already intersected with [0, n_k)
+};
+
+}  // namespace
+
+// ------------------------------------------------------------------------ lifetime
+Executor::Executor(int ndev, const int* ordinals) : R_(ndev) {
+  if (ndev < 1 || ndev > 64) throw Failure(DCPX_ERROR, "dcpx_create: 1..64 devices supported");
+  ordinals_.assign(ordinals, ordinals + ndev);
+  int count = 0;
+  CUDA_OK(cudaGetDeviceCount(&count));
+  for (int o : ordinals_)
+    if (o < 0 || o >= count) throw Failure(DCPX_ERROR, "dcpx_create: bad CUDA ordinal " + std::to_string(o));
+  dev_.resize(static_cast<size_t>(ndev));
+  std::set<int> distinct(ordinals_.begin(), ordinals_.end());
+  for (int a : distinct)
+    for (int b : distinct)
+      if (a != b) {
+        int can = 0;
+        cudaDeviceCanAccessPeer(&can, a, b);
+        if (can) {
+          DeviceGuard g(a);
+          cudaError_t e = cudaDeviceEnablePeerAccess(b, 0);
+          if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled)
+            throw Failure(DCPX_CUDA_ERROR, "cudaDeviceEnablePeerAccess failed");
+          cudaGetLastError();
+        }
+      }
+  for (int d = 0; d < R_; ++d) {
+    DeviceGuard g(ordinals_[d]);
+    dev_[d].ordinal = ordinals_[d];
+    CUDA_OK(cudaStreamCreateWithFlags(&dev_[d].cs, cudaStreamNonBlocking));
+    CUDA_OK(cudaStreamCreateWithFlags(&dev_[d].ms, cudaStreamNonBlocking));
+    CUDA_OK(cudaEventCreate(&dev_[d].t0));
+    CUDA_OK(cudaEventCreate(&dev_[d].t1));
+  }
+}
+
+Executor::~Executor() {
+  for (auto& d : dev_) {
+    DeviceGuard g(d.ordinal);
+    if (d.cs) cudaStreamSynchronize(d.cs);
+    if (d.ms) cudaStreamSynchronize(d.ms);
+  }
+  free_all();
+  for (auto& d : dev_) {
+    DeviceGuard g(d.ordinal);
+    for (auto e : d.events) cudaEventDestroy(e);
+    if (d.t0) cudaEventDestroy(d.t0);
+    if (d.t1) cudaEventDestroy(d.t1);
+    if (d.cs) cudaStreamDestroy(d.cs);
+    if (d.ms) cudaStreamDestroy(d.ms);
+  }
+}
+
+void Executor::free_all() {
+  for (size_t i = 0; i < allocs_.size(); ++i) {
+    DeviceGuard g(alloc_dev_[i]);
+    cudaFree(allocs_[i]);
+  }
+  allocs_.clear();
+  alloc_dev_.clear();
+}
+
+void* Executor::alloc(int d, size_t bytes) {
+  DeviceGuard g(dev_[d].ordinal);
+  void* p = nullptr;
+  CUDA_OK(cudaMalloc(&p, std::max<size_t>(bytes, 256)));
+  allocs_.push_back(p);
+  alloc_dev_.push_back(dev_[d].ordinal);
+  return p;
+}
+
+template <class T>
+T* Executor::upload(int d, const std::vector<T>& v) {
+  if (v.empty()) return nullptr;
+  T* p = static_cast<T*>(alloc(d, v.size() * sizeof(T)));
+  DeviceGuard g(dev_[d].ordinal);
+  CUDA_OK(cudaMemcpy(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
+  return p;
+}
+
+template <class J>
+JobList Executor::make_row_jobs(int d, const std::vector<J>& jobs, const std::vector<int>& rows,
+                                int rows_per_block) {
+  JobList L;
+  std::vector<int32_t> job_of_block, first_chunk;
+  for (size_t j = 0; j < jobs.size(); ++j) {
+    first_chunk.push_back(static_cast<int32_t>(job_of_block.size()));
+    const int nb = (rows[j] + rows_per_block - 1) / rows_per_block;
+    for (int b = 0; b < nb; ++b) job_of_block.push_back(static_cast<int32_t>(j));
+  }
+  L.dj.jobs = upload(d, jobs);
+  L.dj.job_of_block = upload(d, job_of_block);
+  L.dj.first_chunk = upload(d, first_chunk);
+  L.dj.n_blocks = static_cast<int32_t>(job_of_block.size());
+  L.dj.n_jobs = static_cast<int32_t>(jobs.size());
+  return L;
+}
+
+JobList Executor::make_jobs(int d, const std::vector<RowCopyJob>& jobs) {
+  std::vector<int> rows;
+  for (const auto& j : jobs) rows.push_back(j.rows);
+  return make_row_jobs(d, jobs, rows, kRowsPerChunk);
+}
+
+cudaEvent_t Executor::event(int d) {
+  auto& D = dev_[d];
+  if (D.next_event == D.events.size()) {
+    DeviceGuard g(D.ordinal);
+    cudaEvent_t e;
+    CUDA_OK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    D.events.push_back(e);
+  }
+  return D.events[D.next_event++];
+}
+
+// ------------------------------------------------------------------------ prepare
+void Executor::prepare(int nplans, const dcpx_plan_view* plans, const dcpx_graph_view* gv,
+                       const dcpx_mask_view* mv) {
+  if (nplans != R_) throw Failure(DCPX_ERROR, "run: plan count does not match topology");  // simexec.hpp:211
+  free_all();
+  in_stage_ = out_stage_ = nullptr;
+  for (auto& d : dev_) {
+    d.prog.clear();
+    d.o_phys.clear();
+  }
+  prepared_ = false;
+  // ---- graph copy
+  g_ = GraphCopy{};
+  g_.H = gv->heads; g_.G = gv->kv_groups; g_.D = gv->head_dim; g_.bpe = gv->bytes_per_element;
+  if (g_.D != kHeadDim) throw Failure(DCPX_UNSUPPORTED, "sm_100a kernels support head_dim 128 only");
+  if (g_.bpe != 2) throw Failure(DCPX_UNSUPPORTED, "bf16 payloads (bytes_per_element 2) only");
+  if (g_.H < 1 || g_.G < 1 || g_.H % g_.G) throw Failure(DCPX_ERROR, "batch: heads must be divisible by kv_groups");
+  g_.seq_lengths.assign(gv->seq_lengths, gv->seq_lengths + gv->num_seqs);
+  g_.block_sizes.assign(gv->block_sizes, gv->block_sizes + gv->num_seqs);
+  g_.seq_offsets.assign(mv->seq_offsets, mv->seq_offsets + gv->num_seqs + 1);
+  for (int s = 0; s < gv->num_seqs; ++s)
+    if (g_.seq_offsets[s + 1] - g_.seq_offsets[s] != g_.seq_lengths[s])
+      throw Failure(DCPX_ERROR, "mask view does not match sequence lengths");
+  g_.ranges.assign(mv->ranges, mv->ranges + 4 * g_.total_tokens());
+  g_.data_blocks.assign(gv->data_blocks, gv->data_blocks + gv->num_data_blocks);
+  g_.comp_blocks.assign(gv->comp_blocks, gv->comp_blocks + gv->num_comp_blocks);
+  int64_t max_rows = 1;
+  for (const auto& db : g_.data_blocks) {
+    if (db.seq < 0 || db.seq >= gv->num_seqs || db.tok_begin < 0 || db.tok_end > g_.seq_lengths[db.seq] ||
+        db.tok_end <= db.tok_begin)
+      throw Failure(DCPX_ERROR, "graph: bad data block " + std::to_string(db.id));
+    max_rows = std::max<int64_t>(max_rows, db.tok_end - db.tok_begin);
+  }
+  const int64_t slot_rows = (max_rows + 127) / 128 * 128;
+
+  // ---- plan copies
+  plans_.assign(static_cast<size_t>(R_), PlanCopy{});
+  for (int d = 0; d < R_; ++d) {
+    const dcpx_plan_view& v = plans[d];
+    PlanCopy& P = plans_[d];
+    if (v.device != d) throw Failure(DCPX_ERROR, "plan " + std::to_string(d) + " has device " + std::to_string(v.device));
+    P.device = v.device;
+    P.divisions = v.divisions;
+    for (int k = 0; k < 3; ++k) P.cap[k] = v.capacity[k];
+    P.res_q.assign(v.resident_q, v.resident_q + v.n_resident_q);
+    P.res_kv.assign(v.resident_kv, v.resident_kv + v.n_resident_kv);
+    P.res_o.assign(v.resident_o, v.resident_o + v.n_resident_o);
+    int64_t n_items = 0, n_srcs = 0, n_copies = 0, n_blocks = 0, n_rows = 0;
+    for (int i = 0; i < v.n_instructions; ++i) {
+      const dcpx_instruction& x = v.instructions[i];
+      Instr I;
+      I.op = x.op; I.division = x.division; I.send = x.send; I.peer = x.peer; I.dst = x.dst;
+      I.count = x.count; I.offset = x.offset;
+      if (x.tag) I.tag = x.tag;
+      if (I.op < 0 || I.op > 4) throw Failure(DCPX_ERROR, "run: unknown instruction");  // simexec.hpp:369
+      if (I.count < 0 || I.offset < 0) throw Failure(DCPX_ERROR, "plan: negative pool range");
+      const int64_t end = I.offset + I.count;
+      if (I.op == DCPX_OP_ATTENTION) n_items = std::max(n_items, end);
+      if (I.op == DCPX_OP_REDUCTION) n_srcs = std::max(n_srcs, end);
+      if (I.op == DCPX_OP_COPY) n_copies = std::max(n_copies, end);
+      if (I.op == DCPX_OP_COMM_LAUNCH) n_blocks = std::max(n_blocks, end);
+      if ((I.op == DCPX_OP_COMM_LAUNCH || I.op == DCPX_OP_COMM_WAIT) && I.tag.empty())
+        throw Failure(DCPX_TAG_MISMATCH, "communication instruction without a tag");
+      P.ins.push_back(std::move(I));
+    }
+    P.items.assign(v.items, v.items + n_items);
+    P.srcs.assign(v.srcs, v.srcs + n_srcs);
+    P.copies.assign(v.copies, v.copies + n_copies);
+    P.blocks.assign(v.blocks, v.blocks + n_blocks);
+    for (const auto& it : P.items)
+      if (it.rows_offset >= 0) n_rows = std::max<int64_t>(n_rows, it.rows_offset + (it.q_end - it.q_begin));
+    if (n_rows) P.rows.assign(v.rows, v.rows + 4 * n_rows);
+  }
+
+  // ---- static verification (verify_plans, plan.hpp:388-475)
+  {
+    struct Side { int device = -1, peer = -1; std::vector<int> blocks; };
+    std::map<std::string, Side> send_side, recv_side;
+    std::map<std::string, int> wait_count;
+    auto kind_of = [&](int block) {
+      if (block < 0 || block >= static_cast<int>(g_.data_blocks.size()))
+        throw Failure(DCPX_ERROR, "plan: bad data block id " + std::to_string(block));
+      return g_.data_blocks[block].kind;
+    };
+    for (const auto& P : plans_) {
+      std::array<std::set<int>, 3> written;
+      for (const auto& r : P.res_q) written[0].insert(r.slot);
+      for (const auto& r : P.res_kv) written[1].insert(r.slot);
+      std::map<std::string, std::vector<std::pair<int, int>>> pending;
+      auto check_slot = [&](int kind, int slot) {
+        if (slot < 0 || slot >= P.cap[kind])
+          throw Failure(DCPX_BUFFER_OVERFLOW, "device " + std::to_string(P.device) + ": slot " + std::to_string(slot) +
+                                                  " outside capacity " + std::to_string(P.cap[kind]));
+      };
+      auto require = [&](int kind, int slot, const char* what) {
+        check_slot(kind, slot);
+        if (!written[kind].count(slot))
+          throw Failure(DCPX_ERROR, "plan verify: device " + std::to_string(P.device) + ": " + what + " reads slot " +
+                                        std::to_string(slot) + " before it is written");
+      };
+      for (const auto& r : P.res_q) { check_slot(0, r.slot); if (kind_of(r.block) != DCPX_KIND_Q) throw Failure(DCPX_ERROR, "resident_q holds a non-Q block"); }
+      for (const auto& r : P.res_kv) { check_slot(1, r.slot); if (kind_of(r.block) != DCPX_KIND_KV) throw Failure(DCPX_ERROR, "resident_kv holds a non-KV block"); }
+      for (const auto& r : P.res_o) { check_slot(2, r.slot); if (kind_of(r.block) != DCPX_KIND_O) throw Failure(DCPX_ERROR, "resident_o holds a non-O block"); }
+      for (const auto& I : P.ins) {
+        if (I.op == DCPX_OP_ATTENTION) {
+          for (int i = 0; i < I.count; ++i) {
+            const auto& it = P.items[I.offset + i];
+            require(0, it.q_slot, "attention");
+            require(1, it.kv_slot, "attention");
+            check_slot(2, it.out_slot);
+            written[2].insert(it.out_slot);
+            if (it.seq < 0 || it.seq >= static_cast<int>(g_.seq_lengths.size()) || it.head < 0 || it.head >= g_.H ||
+                it.q_begin < 0 || it.q_end > g_.seq_lengths[it.seq] || it.q_end <= it.q_begin || it.kv_begin < 0 ||
+                it.kv_end > g_.seq_lengths[it.seq] || it.kv_end <= it.kv_begin || it.q_end - it.q_begin > slot_rows ||
+                it.kv_end - it.kv_begin > slot_rows)
+              throw Failure(DCPX_ERROR, "exec_attention: inconsistent shapes");  // simexec.hpp:35-38
+          }
+        } else if (I.op == DCPX_OP_REDUCTION) {
+          if (I.count < 1) throw Failure(DCPX_ERROR, "exec_reduction: no partials");  // simexec.hpp:81
+          if (I.count > kMaxMergeSrcs) throw Failure(DCPX_UNSUPPORTED, "reduction with more than 64 partials");
+          for (int i = 0; i < I.count; ++i) require(2, P.srcs[I.offset + i], "reduction");
+          check_slot(2, I.dst);
+          written[2].insert(I.dst);
+        } else if (I.op == DCPX_OP_COPY) {
+          for (int i = 0; i < I.count; ++i) {
+            const auto& c = P.copies[I.offset + i];
+            require(2, c.src_slot, "copy");
+            check_slot(2, c.dst_slot);
+            written[2].insert(c.dst_slot);
+          }
+        } else if (I.op == DCPX_OP_COMM_LAUNCH) {
+          if (I.peer < 0 || I.peer >= R_) throw Failure(DCPX_ERROR, "bad peer device");
+          if (I.send) {
+            for (int i = 0; i < I.count; ++i) {
+              const auto& tb = P.blocks[I.offset + i];
+              require(kind_of(tb.block), tb.slot, "send");
+            }
+            auto [it, ins] = send_side.insert({I.tag, {}});
+            if (!ins) throw Failure(DCPX_TAG_MISMATCH, "duplicate send tag " + I.tag);
+            it->second.device = P.device; it->second.peer = I.peer;
+            for (int i = 0; i < I.count; ++i) it->second.blocks.push_back(P.blocks[I.offset + i].block);
+          } else {
+            auto [it, ins] = recv_side.insert({I.tag, {}});
+            if (!ins) throw Failure(DCPX_TAG_MISMATCH, "duplicate recv tag " + I.tag);
+            it->second.device = P.device; it->second.peer = I.peer;
+            for (int i = 0; i < I.count; ++i) {
+              const auto& tb = P.blocks[I.offset + i];
+              const int k = kind_of(tb.block);
+              check_slot(k, tb.slot);
+              it->second.blocks.push_back(tb.block);
+              pending[I.tag].push_back({k, tb.slot});
+            }
+          }
+        } else if (I.op == DCPX_OP_COMM_WAIT) {
+          auto it = pending.find(I.tag);
+          if (it == pending.end())
+            throw Failure(DCPX_TAG_MISMATCH, "device " + std::to_string(P.device) + " waits on tag " + I.tag +
+                                                 " without a posted receive");
+          for (auto [k, s] : it->second) written[k].insert(s);
+          pending.erase(it);
+          ++wait_count[I.tag];
+        }
+      }
+      if (!pending.empty())
+        throw Failure(DCPX_TAG_MISMATCH, "device " + std::to_string(P.device) + " has posted receives never waited on");
+    }
+    for (const auto& [tag, snd] : send_side) {
+      auto it = recv_side.find(tag);
+      if (it == recv_side.end()) continue;  // unmatched sends surface in the lockstep replay
+      if (snd.peer != it->second.device || it->second.peer != snd.device)
+        throw Failure(DCPX_TAG_MISMATCH, "tag " + tag + " connects mismatched peers");
+      if (snd.blocks != it->second.blocks)
+        throw Failure(DCPX_TAG_MISMATCH, "tag " + tag + " transfers mismatched block lists");
+    }
+  }
+
+  // ---- lockstep replay: deadlock / tag errors + the global issue order
+  simulate_order();
+
+  // ---- per-device compile
+  for (int d = 0; d < R_; ++d) {
+    dev_[d].slot_rows = slot_rows;
+    compile_device(d);
+  }
+  // ---- LOCAL transport: precompiled transfer jobs, owned by the receiver
+  for (int d = 0; d < R_; ++d) {
+    for (auto& op : dev_[d].prog) {
+      if (op.kind != OpKind::kCommWait) continue;
+      // find the matching send and recv launches
+      const PlanCopy& P = plans_[d];
+      int recv_i = -1;
+      for (size_t i = 0; i < P.ins.size(); ++i)
+        if (P.ins[i].op == DCPX_OP_COMM_LAUNCH && !P.ins[i].send && P.ins[i].tag == op.tag) recv_i = static_cast<int>(i);
+      const int src_dev = P.ins[recv_i].peer;
+      const PlanCopy& S = plans_[src_dev];
+      int send_i = -1;
+      for (size_t i = 0; i < S.ins.size(); ++i)
+        if (S.ins[i].op == DCPX_OP_COMM_LAUNCH && S.ins[i].send && S.ins[i].tag == op.tag) send_i = static_cast<int>(i);
+      if (send_i < 0) throw Failure(DCPX_DEADLOCK, "no sender for " + op.tag);
+      const Instr& RI = P.ins[recv_i];
+      const Instr& SI = S.ins[send_i];
+      std::vector<RowCopyJob> jobs;
+      const DevState& A = dev_[src_dev];
+      const DevState& B = dev_[d];
+      for (int b = 0; b < RI.count; ++b) {
+        const auto rb = P.blocks[RI.offset + b];
+        const auto sb = S.blocks[SI.offset + b];
+        const auto& db = g_.data_blocks[rb.block];
+        const int rows = static_cast<int>(db.tok_end - db.tok_begin);
+        if (db.kind == DCPX_KIND_Q) {
+          jobs.push_back({reinterpret_cast<const char*>(A.q + sb.slot * slot_rows * 128),
+                          reinterpret_cast<char*>(B.q + rb.slot * slot_rows * 128), 256, 256, rows, 256});
+        } else if (db.kind == DCPX_KIND_KV) {
+          for (int h = 0; h < 2; ++h)
+            jobs.push_back({reinterpret_cast<const char*>(A.kv + (2 * sb.slot + h) * slot_rows * 128),
+                            reinterpret_cast<char*>(B.kv + (2 * rb.slot + h) * slot_rows * 128), 256, 256, rows, 256});
+        } else {
+          const int64_t so = A.o_phys[sb.slot], ro = B.o_phys[rb.slot];
+          jobs.push_back({reinterpret_cast<const char*>(A.o + so * slot_rows * 128),
+                          reinterpret_cast<char*>(B.o + ro * slot_rows * 128), 256, 256, rows, 256});
+          jobs.push_back({reinterpret_cast<const char*>(A.lse + so * slot_rows),
+                          reinterpret_cast<char*>(B.lse + ro * slot_rows), 4 * rows, 4 * rows, 1, 4 * rows});
+        }
+      }
+      op.jobs = make_jobs(d, jobs);
+      op.peer = src_dev;
+    }
+    build_io_jobs(d);
+  }
+  for (int d = 0; d < R_; ++d) {
+    DeviceGuard g(dev_[d].ordinal);
+    CUDA_OK(cudaDeviceSynchronize());
+  }
+  prepared_ = true;
+}
+
+void Executor::simulate_order() {
+  order_.clear();
+  const int T = R_ ? plans_[0].divisions : 0;
+  comm_bytes_.assign(static_cast<size_t>(T) + 1, {});
+  comp_flops_.assign(static_cast<size_t>(T) + 1, std::vector<uint64_t>(static_cast<size_t>(R_), 0));
+  std::vector<size_t> pc(static_cast<size_t>(R_), 0);
+  std::map<std::string, std::pair<int, int>> inbox;  // tag -> (src, dst)
+  std::vector<std::set<std::string>> posted(static_cast<size_t>(R_));
+  while (true) {
+    bool all_done = true, any = false;
+    for (int d = 0; d < R_; ++d) {
+      const auto& P = plans_[d];
+      if (pc[d] >= P.ins.size()) continue;
+      all_done = false;
+      while (pc[d] < P.ins.size()) {
+        const Instr& I = P.ins[pc[d]];
+        if (I.op == DCPX_OP_COMM_WAIT) {
+          auto it = inbox.find(I.tag);
+          if (it == inbox.end()) break;
+          if (it->second.second != d) throw Failure(DCPX_TAG_MISMATCH, "message " + I.tag + " delivered to wrong device");
+          if (!posted[d].count(I.tag))
+            throw Failure(DCPX_TAG_MISMATCH, "device " + std::to_string(d) + " waits on " + I.tag + " without a posted receive");
+          posted[d].erase(I.tag);
+          inbox.erase(it);
+        } else if (I.op == DCPX_OP_COMM_LAUNCH) {
+          if (I.send) {
+            if (!inbox.insert({I.tag, {d, I.peer}}).second)
+              throw Failure(DCPX_TAG_MISMATCH, "duplicate message tag " + I.tag);
+            uint64_t bytes = 0;
+            for (int b = 0; b < I.count; ++b) bytes += g_.data_blocks[P.blocks[I.offset + b].block].size_bytes;
+            if (I.division >= 0 && I.division <= T) comm_bytes_[I.division][{d, I.peer}] += bytes;
+          } else {
+            posted[d].insert(I.tag);
+          }
+        }
+        order_.push_back({d, static_cast<int>(pc[d])});
+        ++pc[d];
+        any = true;
+      }
+    }
+    if (all_done) break;
+    if (!any) {
+      std::string msg = "deadlock: ";
+      for (int d = 0; d < R_; ++d)
+        if (pc[d] < plans_[d].ins.size() && plans_[d].ins[pc[d]].op == DCPX_OP_COMM_WAIT)
+          msg += "device " + std::to_string(d) + " waits on " + plans_[d].ins[pc[d]].tag + "; ";
+      throw Failure(DCPX_DEADLOCK, msg);  // simexec.hpp:384-394
+    }
+  }
+  if (!inbox.empty()) throw Failure(DCPX_TAG_MISMATCH, "messages left undelivered at termination");  // :396-397
+}
+
+// Does any instruction at index >= start read O slot `slot` before overwriting it?
+static bool o_read_before_write(const PlanCopy& P, const GraphCopy& g, size_t start, int slot) {
+  for (size_t i = start; i < P.ins.size(); ++i) {
+    const Instr& I = P.ins[i];
+    if (I.op == DCPX_OP_ATTENTION) {
+      for (int k = 0; k < I.count; ++k)
+        if (P.items[I.offset + k].out_slot == slot) return false;
+    } else if (I.op == DCPX_OP_REDUCTION) {
+      for (int k = 0; k < I.count; ++k)
+        if (P.srcs[I.offset + k] == slot) return true;
+      if (I.dst == slot) return false;
+    } else if (I.op == DCPX_OP_COPY) {
+      for (int k = 0; k < I.count; ++k)
+        if (P.copies[I.offset + k].src_slot == slot) return true;
+      for (int k = 0; k < I.count; ++k)
+        if (P.copies[I.offset + k].dst_slot == slot) return false;
+    } else if (I.op == DCPX_OP_COMM_LAUNCH) {
+      for (int k = 0; k < I.count; ++k) {
+        const auto& tb = P.blocks[I.offset + k];
+        if (g.data_blocks[tb.block].kind == DCPX_KIND_O && tb.slot == slot) return I.send ? true : false;
+      }
+    }
+  }
+  return false;
+}
+
+// Does any instruction at index >= start touch O slot `slot` at all?
+static bool o_touched(const PlanCopy& P, const GraphCopy& g, size_t start, int slot) {
+  for (size_t i = start; i < P.ins.size(); ++i) {
+    const Instr& I = P.ins[i];
+    if (I.op == DCPX_OP_ATTENTION) {
+      for (int k = 0; k < I.count; ++k)
+        if (P.items[I.offset + k].out_slot == slot) return true;
+    } else if (I.op == DCPX_OP_REDUCTION) {
+      if (I.dst == slot) return true;
+      for (int k = 0; k < I.count; ++k)
+        if (P.srcs[I.offset + k] == slot) return true;
+    } else if (I.op == DCPX_OP_COPY) {
+      for (int k = 0; k < I.count; ++k)
+        if (P.copies[I.offset + k].src_slot == slot || P.copies[I.offset + k].dst_slot == slot) return true;
+    } else if (I.op == DCPX_OP_COMM_LAUNCH) {
+      for (int k = 0; k < I.count; ++k) {
+        const auto& tb = P.blocks[I.offset + k];
+        if (g.data_blocks[tb.block].kind == DCPX_KIND_O && tb.slot == slot) return true;
+      }
+    }
+  }
+  return false;
+}
+
+struct AttnGroup {
+  std::vector<int> items;  // indices into P.items
+  int target = 0;          // O slot receiving the merged result
+  bool merge_prev = false;
+};
+
+void Executor::compile_device(int d) {
+  PlanCopy& P = plans_[d];
+  DevState& D = dev_[d];
+  const int64_t SR = D.slot_rows;
+  D.prog.assign(P.ins.size(), Op{});
+
+  // ---- 1. fusion decisions for attention + reductions
+  std::vector<bool> fused_red(P.ins.size(), false);
+  std::vector<std::vector<AttnGroup>> groups_of(P.ins.size());
+  std::vector<int> o_written;  // O slots written by the program
+  for (size_t a = 0; a < P.ins.size(); ++a) {
+    const Instr& I = P.ins[a];
+    if (I.op != DCPX_OP_ATTENTION) continue;
+    std::map<int, int> out2item;
+    for (int k = 0; k < I.count; ++k) {
+      const int idx = static_cast<int>(I.offset) + k;
+      if (!out2item.insert({P.items[idx].out_slot, idx}).second)
+        throw Failure(DCPX_ERROR, "attention instruction writes one slot twice");
+    }
+    std::set<int> covered;
+    auto& groups = groups_of[a];
+    if (opt.fuse_reductions) {
+      for (size_t r = a + 1; r < P.ins.size() && P.ins[r].op == DCPX_OP_REDUCTION; ++r) {
+        const Instr& Rd = P.ins[r];
+        std::vector<int> srcs(P.srcs.begin() + Rd.offset, P.srcs.begin() + Rd.offset + Rd.count);
+        const bool dst_in_srcs = std::find(srcs.begin(), srcs.end(), Rd.dst) != srcs.end();
+        if (!dst_in_srcs) continue;
+        bool ok = true;
+        AttnGroup grp;
+        grp.target = Rd.dst;
+        std::set<int> seen;
+        for (int s : srcs) {
+          if (!seen.insert(s).second) { ok = false; break; }
+          auto it = out2item.find(s);
+          if (it == out2item.end()) {
+            if (s != Rd.dst) { ok = false; break; }
+            continue;  // existing accumulator (earlier division)
+          }
+          if (covered.count(it->second)) { ok = false; break; }
+          grp.items.push_back(it->second);
+        }
+        if (!ok || grp.items.empty()) continue;
+        grp.merge_prev = !out2item.count(Rd.dst);
+        const auto& i0 = P.items[grp.items[0]];
+        for (int idx : grp.items) {
+          const auto& x = P.items[idx];
+          if (x.q_slot != i0.q_slot || x.q_begin != i0.q_begin || x.q_end != i0.q_end || x.seq != i0.seq) ok = false;
+        }
+        for (int s : srcs)
+          if (s != Rd.dst && o_read_before_write(P, g_, r + 1, s)) ok = false;
+        // the attention's other items must not read the accumulator being merged
+        if (!ok) continue;
+        for (int idx : grp.items) covered.insert(idx);
+        groups.push_back(grp);
+        fused_red[r] = true;
+      }
+    }
+    for (int k = 0; k < I.count; ++k) {
+      const int idx = static_cast<int>(I.offset) + k;
+      if (covered.count(idx)) continue;
+      AttnGroup grp;
+      grp.items = {idx};
+      grp.target = P.items[idx].out_slot;
+      groups.push_back(grp);
+    }
+    for (const auto& grp : groups) o_written.push_back(grp.target);
+  }
+
+  // ---- 2. copy remaps and the physical O slot map
+  std::vector<int> remap_dst2src(static_cast<size_t>(P.cap[2]), -1);
+  std::vector<bool> copy_remapped(P.ins.size(), false);
+  for (size_t c = 0; c < P.ins.size(); ++c) {
+    const Instr& I = P.ins[c];
+    if (I.op != DCPX_OP_COPY || !opt.remap_copies) continue;
+    bool ok = true;
+    std::set<int> srcs, dsts;
+    for (int k = 0; k < I.count; ++k) {
+      const auto& ci = P.copies[I.offset + k];
+      if (!srcs.insert(ci.src_slot).second || !dsts.insert(ci.dst_slot).second) ok = false;
+      if (o_touched(P, g_, c + 1, ci.src_slot) || o_touched(P, g_, c + 1, ci.dst_slot)) ok = false;
+    }
+    for (int s : srcs)
+      if (dsts.count(s)) ok = false;
+    // the destination must be a resident output slot that nothing else reads
+    if (!ok) continue;
+    copy_remapped[c] = true;
+    for (int k = 0; k < I.count; ++k) remap_dst2src[P.copies[I.offset + k].dst_slot] = P.copies[I.offset + k].src_slot;
+  }
+  std::vector<bool> o_used(static_cast<size_t>(P.cap[2]), false);
+  for (int s : o_written) o_used[s] = true;
+  for (size_t i = 0; i < P.ins.size(); ++i) {
+    const Instr& I = P.ins[i];
+    if (I.op == DCPX_OP_REDUCTION && !fused_red[i]) {
+      o_used[I.dst] = true;
+      for (int k = 0; k < I.count; ++k) o_used[P.srcs[I.offset + k]] = true;
+    } else if (I.op == DCPX_OP_COPY) {
+      for (int k = 0; k < I.count; ++k) {
+        o_used[P.copies[I.offset + k].src_slot] = true;
+        if (!copy_remapped[i]) o_used[P.copies[I.offset + k].dst_slot] = true;
+      }
+    } else if (I.op == DCPX_OP_COMM_LAUNCH) {
+      for (int k = 0; k < I.count; ++k) {
+        const auto& tb = P.blocks[I.offset + k];
+        if (g_.data_blocks[tb.block].kind == DCPX_KIND_O) o_used[tb.slot] = true;
+      }
+    }
+  }
+  for (const auto& r : P.res_o) {
+    const int src = remap_dst2src[r.slot];
+    o_used[src >= 0 ? src : r.slot] = true;
+  }
+  D.o_phys.assign(static_cast<size_t>(P.cap[2]), -1);
+  int64_t n_o = 0;
+  for (int s = 0; s < P.cap[2]; ++s)
+    if (o_used[s]) D.o_phys[s] = static_cast<int32_t>(n_o++);
+  D.cap_q = P.cap[0];
+  D.cap_kv = P.cap[1];
+  D.cap_o = n_o;
+
+  // ---- 3. arenas (zero-initialised: stale rows stay finite) and tensor maps
+  {
+    DeviceGuard gd(D.ordinal);
+    D.q = static_cast<__nv_bfloat16*>(alloc(d, std::max<int64_t>(1, D.cap_q) * SR * 256));
+    D.kv = static_cast<__nv_bfloat16*>(alloc(d, std::max<int64_t>(1, D.cap_kv) * 2 * SR * 256));
+    D.o = static_cast<__nv_bfloat16*>(alloc(d, std::max<int64_t>(1, D.cap_o) * SR * 256));
+    D.lse = static_cast<float*>(alloc(d, std::max<int64_t>(1, D.cap_o) * SR * 4));
+    CUDA_OK(cudaMemset(D.q, 0, std::max<int64_t>(1, D.cap_q) * SR * 256));
+    CUDA_OK(cudaMemset(D.kv, 0, std::max<int64_t>(1, D.cap_kv) * 2 * SR * 256));
+    CUDA_OK(cudaMemset(D.o, 0, std::max<int64_t>(1, D.cap_o) * SR * 256));
+    CUDA_OK(cudaMemset(D.lse, 0, std::max<int64_t>(1, D.cap_o) * SR * 4));
+    D.tm_q = make_tmap(D.q, std::max<int64_t>(1, D.cap_q) * SR);
+    D.tm_kv = make_tmap(D.kv, std::max<int64_t>(1, D.cap_kv) * 2 * SR);
+    std::vector<int32_t> ranges = g_.ranges;
+    ranges.insert(ranges.end(), P.rows.begin(), P.rows.end());
+    if (ranges.empty()) ranges.assign(4, 0);
+    D.ranges = upload(d, ranges);
+  }
+
+  // ---- 4. per-instruction device ops
+  const int64_t TT = g_.total_tokens();
+  for (size_t i = 0; i < P.ins.size(); ++i) {
+    const Instr& I = P.ins[i];
+    Op& op = D.prog[i];
+    op.division = I.division;
+    op.instr = static_cast<int>(i);
+    switch (I.op) {
+      case DCPX_OP_ATTENTION: {
+        op.kind = OpKind::kFwdAttn;
+        std::vector<FwdUnit> units;
+        std::vector<FwdStep> steps;
+        std::vector<ItemMask> masks;
+        std::vector<int64_t> unit_cost;
+        std::map<int, int> mask_of_item;
+        for (const auto& grp : groups_of[i]) {
+          const auto& i0 = P.items[grp.items[0]];
+          const int n_q = static_cast<int>(i0.q_end - i0.q_begin);
+          const int n_pairs = (n_q + 255) / 256;
+          const int n_qt = (n_q + 127) / 128;
+          // per item: classification table [q tile][kv sub-tile]
+          struct ItemCls { int nks; std::vector<uint8_t> cls; int mask; };
+          std::vector<ItemCls> ic;
+          for (int idx : grp.items) {
+            const auto& it = P.items[idx];
+            const int n_k = static_cast<int>(it.kv_end - it.kv_begin);
+            const int nks = (n_k + 127) / 128;
+            ItemMask im{};
+            im.n_k = n_k;
+            const int32_t* rg;
+            if (it.rows_offset >= 0) {
+              im.range_row0 = TT + it.rows_offset;
+              im.kv_shift = 0;
+              rg = P.rows.data() + 4 * it.rows_offset;
+            } else {
+              im.range_row0 = g_.seq_offsets[it.seq] + it.q_begin;
+              im.kv_shift = it.kv_begin;
+              rg = g_.ranges.data() + 4 * (g_.seq_offsets[it.seq] + it.q_begin);
+            }
+            ItemCls c;
+            c.nks = nks;
+            c.mask = static_cast<int>(masks.size());
+            masks.push_back(im);
+            std::vector<uint8_t> all_full(static_cast<size_t>(n_qt) * nks, 1), any(static_cast<size_t>(n_qt) * nks, 0);
+            uint64_t pairs = 0;
+            for (int r = 0; r < n_q; ++r) {
+              RelRange rr;
+              const int64_t sh = im.kv_shift;
+              rr.b0 = static_cast<int32_t>(std::max<int64_t>(rg[4 * r] - sh, 0));
+              rr.e0 = static_cast<int32_t>(std::min<int64_t>(rg[4 * r + 1] - sh, n_k));
+              rr.b1 = static_cast<int32_t>(std::max<int64_t>(rg[4 * r + 2] - sh, 0));
+              rr.e1 = static_cast<int32_t>(std::min<int64_t>(rg[4 * r + 3] - sh, n_k));
+              if (it.rows_offset >= 0 && (rg[4 * r] < 0 || rg[4 * r + 1] > n_k || rg[4 * r + 2] < 0 || rg[4 * r + 3] > n_k) &&
+                  (rg[4 * r + 1] > rg[4 * r] || rg[4 * r + 3] > rg[4 * r + 2]))
+                throw Failure(DCPX_ERROR, "exec_attention: range outside kv tile");  // simexec.hpp:53
+              if (rr.e0 > rr.b0) pairs += rr.e0 - rr.b0;
+              if (rr.e1 > rr.b1) pairs += rr.e1 - rr.b1;
+              const int qt = r / 128;
+              for (int ks = 0; ks < nks; ++ks) {
+                const int c0 = ks * 128, c1 = std::min(n_k, c0 + 128);
+                const bool full = (c1 - c0 == 128) && ((rr.b0 <= c0 && rr.e0 >= c1) || (rr.b1 <= c0 && rr.e1 >= c1));
+                const bool hit = (rr.e0 > rr.b0 && rr.b0 < c1 && rr.e0 > c0) || (rr.e1 > rr.b1 && rr.b1 < c1 && rr.e1 > c0);
+                if (!full) all_full[qt * nks + ks] = 0;
+                if (hit) any[qt * nks + ks] = 1;
+              }
+            }
+            op.flops += 4ull * pairs * static_cast<uint64_t>(g_.D);
+            c.cls.resize(static_cast<size_t>(n_qt) * nks);
+            for (size_t k = 0; k < c.cls.size(); ++k)
+              c.cls[k] = !any[k] ? kTileEmpty : (all_full[k] ? kTileFull : kTilePartial);
+            ic.push_back(std::move(c));
+          }
+          for (int pr = 0; pr < n_pairs; ++pr) {
+            FwdUnit U{};
+            U.q_row0 = static_cast<int32_t>(i0.q_slot * SR + 256 * pr);
+            U.n_rows = std::min(256, n_q - 256 * pr);
+            U.out_row0 = static_cast<int32_t>(D.o_phys[grp.target] * SR + 256 * pr);
+            U.flags = grp.merge_prev ? 1 : 0;
+            U.q_local0 = 256 * pr;
+            U.step_begin = static_cast<int32_t>(steps.size());
+            int64_t cost = 0;
+            for (size_t gi = 0; gi < grp.items.size(); ++gi) {
+              const auto& it = P.items[grp.items[gi]];
+              const auto& c = ic[gi];
+              for (int ks = 0; ks < c.nks; ++ks) {
+                const uint32_t c0 = c.cls[(2 * pr) * c.nks + ks];
+                const uint32_t c1 = (2 * pr + 1 < n_qt) ? c.cls[(2 * pr + 1) * c.nks + ks] : kTileEmpty;
+                if (!c0 && !c1) continue;
+                FwdStep S{};
+                S.kv_row0 = static_cast<int32_t>(2 * it.kv_slot * SR + 128 * ks);
+                S.col0 = 128 * ks;
+                S.item = c.mask;
+                S.cls = c0 | (c1 << 2);
+                steps.push_back(S);
+                cost += (c0 ? 1 : 0) + (c1 ? 1 : 0);
+              }
+            }
+            U.step_count = static_cast<int32_t>(steps.size()) - U.step_begin;
+            units.push_back(U);
+            unit_cost.push_back(cost * 1000 + U.n_rows);
+          }
+        }
+        // longest-processing-time-first order for the static round-robin schedule
+        std::vector<size_t> order(units.size());
+        std::iota(order.begin(), order.end(), 0);
+        std::stable_sort(order.begin(), order.end(), [&](size_t a, size_t b) { return unit_cost[a] > unit_cost[b]; });
+        std::vector<FwdUnit> sorted;
+        for (size_t k : order) sorted.push_back(units[k]);
+        op.units = upload(d, sorted);
+        op.steps = upload(d, steps);
+        op.items = upload(d, masks);
+        op.num_units = static_cast<int>(sorted.size());
+        op.grid = std::min(op.num_units, num_sms(D.ordinal));
+        if (I.division >= 0 && I.division < static_cast<int>(comp_flops_.size())) comp_flops_[I.division][d] += op.flops;
+        break;
+      }
+      case DCPX_OP_REDUCTION: {
+        if (fused_red[i]) { op.kind = OpKind::kNop; break; }
+        op.kind = OpKind::kMerge;
+        MergeJob J{};
+        J.dst_row0 = static_cast<int32_t>(D.o_phys[I.dst] * SR);
+        J.n_rows = static_cast<int32_t>(SR);
+        J.src_begin = 0;
+        J.n_src = I.count;
+        std::vector<int32_t> srows;
+        for (int k = 0; k < I.count; ++k) srows.push_back(static_cast<int32_t>(D.o_phys[P.srcs[I.offset + k]] * SR));
+        op.src_rows = upload(d, srows);
+        op.jobs = make_row_jobs(d, std::vector<MergeJob>{J}, std::vector<int>{J.n_rows}, 16);
+        break;
+      }
+      case DCPX_OP_COPY: {
+        if (copy_remapped[i]) { op.kind = OpKind::kNop; break; }
+        op.kind = OpKind::kCopy;
+        std::vector<RowCopyJob> jobs;
+        for (int k = 0; k < I.count; ++k) {
+          const auto& ci = P.copies[I.offset + k];
+          const int64_t s = D.o_phys[ci.src_slot], t = D.o_phys[ci.dst_slot];
+          jobs.push_back({reinterpret_cast<const char*>(D.o + s * SR * 128), reinterpret_cast<char*>(D.o + t * SR * 128),
+                          256, 256, static_cast<int32_t>(SR), 256});
+          jobs.push_back({reinterpret_cast<const char*>(D.lse + s * SR), reinterpret_cast<char*>(D.lse + t * SR),
+                          static_cast<int64_t>(SR) * 4, static_cast<int64_t>(SR) * 4, 1, static_cast<int32_t>(SR * 4)});
+        }
+        op.jobs = make_jobs(d, jobs);
+        break;
+      }
+      case DCPX_OP_COMM_LAUNCH: {
+        op.kind = OpKind::kCommLaunch;
+        op.send = I.send;
+        op.peer = I.peer;
+        op.tag = I.tag;
+        op.blocks.assign(P.blocks.begin() + I.offset, P.blocks.begin() + I.offset + I.count);
+        for (const auto& tb : op.blocks) op.bytes += g_.data_blocks[tb.block].size_bytes;
+        if (I.send) {  // snapshot semantics: the sent slots must not be rewritten afterwards
+          for (const auto& tb : op.blocks)
+            if (g_.data_blocks[tb.block].kind == DCPX_KIND_O && o_touched(P, g_, i + 1, tb.slot)) {
+              for (size_t k = i + 1; k < P.ins.size(); ++k) {
+                const Instr& X = P.ins[k];
+                bool writes = (X.op == DCPX_OP_REDUCTION && X.dst == tb.slot);
+                for (int q = 0; X.op == DCPX_OP_ATTENTION && q < X.count; ++q)
+                  writes |= P.items[X.offset + q].out_slot == tb.slot;
+                if (writes) throw Failure(DCPX_UNSUPPORTED, "plan overwrites a slot with an in-flight send");
+              }
+            }
+        }
+        break;
+      }
+      case DCPX_OP_COMM_WAIT:
+        op.kind = OpKind::kCommWait;
+        op.tag = I.tag;
+        break;
+    }
+  }
+  // final output slots (after copy remaps)
+  D.final_o_slot.clear();
+  for (const auto& r : P.res_o) {
+    const int src = remap_dst2src[r.slot];
+    D.final_o_slot.push_back(D.o_phys[src >= 0 ? src : r.slot]);
+  }
+}
+
+void Executor::build_io_jobs(int d) {
+  const PlanCopy& P = plans_[d];
+  DevState& D = dev_[d];
+  const int64_t SR = D.slot_rows, H = g_.H, G = g_.G, TT = g_.total_tokens();
+  std::vector<RowCopyJob> sq, sk, sv, go, gl;
+  for (const auto& r : P.res_q) {
+    const auto& db = g_.data_blocks[r.block];
+    const int64_t tok = g_.seq_offsets[db.seq] + db.tok_begin;
+    sq.push_back({reinterpret_cast<const char*>((tok * H + db.head) * 256),
+                  reinterpret_cast<char*>(D.q + r.slot * SR * 128), H * 256, 256,
+                  static_cast<int32_t>(db.tok_end - db.tok_begin), 256});
+  }
+  for (const auto& r : P.res_kv) {
+    const auto& db = g_.data_blocks[r.block];
+    const int64_t tok = g_.seq_offsets[db.seq] + db.tok_begin;
+    for (int h = 0; h < 2; ++h)
+      (h ? sv : sk).push_back({reinterpret_cast<const char*>((tok * G + db.head) * 256),
+                               reinterpret_cast<char*>(D.kv + (2 * r.slot + h) * SR * 128), G * 256, 256,
+                               static_cast<int32_t>(db.tok_end - db.tok_begin), 256});
+  }
+  for (size_t i = 0; i < P.res_o.size(); ++i) {
+    const auto& db = g_.data_blocks[P.res_o[i].block];
+    const int64_t tok = g_.seq_offsets[db.seq] + db.tok_begin;
+    const int64_t phys = D.final_o_slot[i];
+    const int rows = static_cast<int>(db.tok_end - db.tok_begin);
+    go.push_back({reinterpret_cast<const char*>(D.o + phys * SR * 128), reinterpret_cast<char*>((tok * H + db.head) * 256),
+                  256, H * 256, rows, 256});
+    gl.push_back({reinterpret_cast<const char*>(D.lse + phys * SR), reinterpret_cast<char*>((db.head * TT + tok) * 4),
+                  4 * rows, 4 * rows, 1, 4 * rows});
+  }
+  D.scatter_q = make_jobs(d, sq);
+  D.scatter_k = make_jobs(d, sk);
+  D.scatter_v = make_jobs(d, sv);
+  D.gather_o = make_jobs(d, go);
+  D.gather_lse = make_jobs(d, gl);
+}
+
+// ------------------------------------------------------------------------ execution
+void Executor::load_inputs(const void* q, const void* k, const void* v, bool host) {
+  if (!prepared_) throw Failure(DCPX_ERROR, "dcpx_load_inputs before dcpx_prepare");
+  const int64_t TT = g_.total_tokens();
+  const void *dq = q, *dk = k, *dv = v;
+  if (host) {
+    // stage once on the first device; peers read it over NVLink
+    DevState& D0 = dev_[0];
+    DeviceGuard gd(D0.ordinal);
+    const size_t bq = TT * g_.H * 256, bk = TT * g_.G * 256;
+    if (!in_stage_) in_stage_ = static_cast<char*>(alloc(0, bq + 2 * bk));
+    char* buf = in_stage_;
+    CUDA_OK(cudaMemcpyAsync(buf, q, bq, cudaMemcpyHostToDevice, D0.cs));
+    CUDA_OK(cudaMemcpyAsync(buf + bq, k, bk, cudaMemcpyHostToDevice, D0.cs));
+    CUDA_OK(cudaMemcpyAsync(buf + bq + bk, v, bk, cudaMemcpyHostToDevice, D0.cs));
+    cudaEvent_t e = event(0);
+    CUDA_OK(cudaEventRecord(e, D0.cs));
+    for (int d = 1; d < R_; ++d) {
+      DeviceGuard g2(dev_[d].ordinal);
+      CUDA_OK(cudaStreamWaitEvent(dev_[d].cs, e, 0));
+    }
+    dq = buf; dk = buf + bq; dv = buf + bq + bk;
+  }
+  for (int d = 0; d < R_; ++d) {
+    DevState& D = dev_[d];
+    DeviceGuard gd(D.ordinal);
+    launch_row_copy(D.scatter_q.dj, D.cs, reinterpret_cast<int64_t>(dq), 0);
+    launch_row_copy(D.scatter_k.dj, D.cs, reinterpret_cast<int64_t>(dk), 0);
+    launch_row_copy(D.scatter_v.dj, D.cs, reinterpret_cast<int64_t>(dv), 0);
+    CUDA_OK(cudaGetLastError());
+  }
+}
+
+void Executor::forward(void* o_out, float* lse_out, dcpx_report* rep, bool host) {
+  if (!prepared_) throw Failure(DCPX_ERROR, "dcpx_forward before dcpx_prepare");
+  const int64_t TT = g_.total_tokens();
+  for (auto& D : dev_) {
+    D.next_event = 0;
+    D.launches = 0;
+    DeviceGuard gd(D.ordinal);
+    if (opt.timing) CUDA_OK(cudaEventRecord(D.t0, D.cs));
+  }
+  std::map<std::string, cudaEvent_t> send_ev, recv_ev;
+  for (const auto& [d, i] : order_) {
+    DevState& D = dev_[d];
+    Op& op = D.prog[i];
+    DeviceGuard gd(D.ordinal);
+    switch (op.kind) {
+      case OpKind::kFwdAttn: {
+        if (!op.num_units) break;
+        FwdParams p{};
+        p.units = op.units; p.steps = op.steps; p.items = op.items; p.ranges = D.ranges;
+        p.o_arena = D.o; p.lse_arena = D.lse; p.num_units = op.num_units;
+        p.slot_rows = static_cast<int32_t>(D.slot_rows);
+        p.scale_log2 = static_cast<float>(1.4426950408889634 / std::sqrt(static_cast<double>(g_.D)));
+        launch_attn_fwd(D.tm_q, D.tm_kv, p, op.grid, D.cs);
+        ++D.launches;
+        break;
+      }
+      case OpKind::kMerge:
+        launch_merge(op.jobs.dj, op.src_rows, D.o, D.lse, D.cs);
+        ++D.launches;
+        break;
+      case OpKind::kCopy:
+        launch_row_copy(op.jobs.dj, D.cs);
+        ++D.launches;
+        break;
+      case OpKind::kCommLaunch: {
+        cudaEvent_t e = event(d);
+        CUDA_OK(cudaEventRecord(e, D.cs));
+        (op.send ? send_ev : recv_ev)[op.tag] = e;
+        break;
+      }
+      case OpKind::kCommWait: {
+        CUDA_OK(cudaStreamWaitEvent(D.ms, send_ev.at(op.tag), 0));
+        CUDA_OK(cudaStreamWaitEvent(D.ms, recv_ev.at(op.tag), 0));
+        launch_row_copy(op.jobs.dj, D.ms);
+        ++D.launches;
+        cudaEvent_t e = event(d);
+        CUDA_OK(cudaEventRecord(e, D.ms));
+        CUDA_OK(cudaStreamWaitEvent(D.cs, e, 0));
+        break;
+      }
+      case OpKind::kNop:
+        break;
+    }
+  }
+  // output assembly (simexec.hpp:403-421) into the caller's packed buffers
+  char* o_dev = static_cast<char*>(o_out);
+  char* l_dev = reinterpret_cast<char*>(lse_out);
+  if (host && (o_out || lse_out)) {
+    if (!out_stage_) out_stage_ = static_cast<char*>(alloc(0, TT * g_.H * 256 + TT * g_.H * 4));
+    char* buf = out_stage_;
+    o_dev = o_out ? buf : nullptr;
+    l_dev = lse_out ? buf + TT * g_.H * 256 : nullptr;
+  }
+  for (int d = 0; d < R_; ++d) {
+    DevState& D = dev_[d];
+    DeviceGuard gd(D.ordinal);
+    if (o_dev) { launch_row_copy(D.gather_o.dj, D.cs, 0, reinterpret_cast<int64_t>(o_dev)); ++D.launches; }
+    if (l_dev) { launch_row_copy(D.gather_lse.dj, D.cs, 0, reinterpret_cast<int64_t>(l_dev)); ++D.launches; }
+    if (opt.timing) CUDA_OK(cudaEventRecord(D.t1, D.cs));
+    CUDA_OK(cudaGetLastError());
+  }
+  if (host && (o_out || lse_out)) {
+    DevState& D0 = dev_[0];
+    DeviceGuard gd(D0.ordinal);
+    for (int d = 1; d < R_; ++d) {
+      cudaEvent_t e = event(d);
+      DeviceGuard g2(dev_[d].ordinal);
+      CUDA_OK(cudaEventRecord(e, dev_[d].cs));
+      DeviceGuard g3(D0.ordinal);
+      CUDA_OK(cudaStreamWaitEvent(D0.cs, e, 0));
+    }
+    if (o_out) CUDA_OK(cudaMemcpyAsync(o_out, o_dev, TT * g_.H * 256, cudaMemcpyDeviceToHost, D0.cs));
+    if (lse_out) CUDA_OK(cudaMemcpyAsync(lse_out, l_dev, TT * g_.H * 4, cudaMemcpyDeviceToHost, D0.cs));
+    CUDA_OK(cudaStreamSynchronize(D0.cs));
+  }
+  if (rep) {
+    std::memset(rep, 0, sizeof(*rep));
+    rep->devices = R_;
+    rep->stages = static_cast<int32_t>(comm_bytes_.size());
+    std::vector<double> comp_t(comm_bytes_.size(), 0), comm_t(comm_bytes_.size(), 0);
+    for (size_t t = 0; t < comm_bytes_.size(); ++t) {
+      for (const auto& [link, bytes] : comm_bytes_[t]) {
+        rep->total_bytes += bytes;
+        rep->per_device_send[link.first] += bytes;
+        rep->per_device_recv[link.second] += bytes;
+        comm_t[t] = std::max(comm_t[t], bytes ? 5e-6 + static_cast<double>(bytes) / 600e9 : 0.0);  // link_time, schedule.hpp:209-215
+      }
+      for (int d = 0; d < R_; ++d) {
+        rep->total_flops += comp_flops_[t][d];
+        comp_t[t] = std::max(comp_t[t], static_cast<double>(comp_flops_[t][d]) / 312e12);  // CostParams, schedule.hpp:173-175
+      }
+    }
+    // pipeline_makespan (schedule.hpp:192-207)
+    double start_prev = 0, finish = 0;
+    for (size_t t = 0; t < comm_t.size(); ++t) {
+      const double start = t == 0 ? 0 : std::max(finish, start_prev + comm_t[t]);
+      start_prev = start;
+      finish = start + comp_t[t];
+    }
+    rep->makespan = finish;
+    rep->wire_bytes = rep->total_bytes;
+    for (int d = 0; d < R_; ++d) rep->kernel_launches += dev_[d].launches;
+    if (opt.timing) {
+      double mx = 0;
+      for (auto& D : dev_) {
+        DeviceGuard gd(D.ordinal);
+        CUDA_OK(cudaEventSynchronize(D.t1));
+        float ms = 0;
+        CUDA_OK(cudaEventElapsedTime(&ms, D.t0, D.t1));
+        mx = std::max<double>(mx, ms);
+      }
+      rep->device_ms = mx;
+    }
+  }
+}
+
+void Executor::synchronize() {
+  for (auto& D : dev_) {
+    DeviceGuard gd(D.ordinal);
+    CUDA_OK(cudaStreamSynchronize(D.cs));
+    CUDA_OK(cudaStreamSynchronize(D.ms));
+  }
+}
+
+void Executor::debug_arena(int d, int kind, void** ptr, int64_t* rows) {
+  if (d < 0 || d >= R_) throw Failure(DCPX_ERROR, "bad device");
+  const DevState& D = dev_[d];
+  *rows = D.slot_rows;
+  switch (kind) {
+    case 0: *ptr = D.q; break;
+    case 1: *ptr = D.kv; break;
+    case 2: *ptr = D.o; break;
+    case 3: *ptr = D.lse; break;
+    default: throw Failure(DCPX_ERROR, "bad arena kind");
+  }
+}
+
+}  // namespace dcpx

@@ -1,0 +1,150 @@
+// executor.h — host side of the B200 DCP executor (C++; the C ABI in capi.cu wraps it).
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <map>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/dcpx.h"
+#include "movers.h"
+#include "program.h"
+
+namespace dcpx {
+
+// Exception carrying a dcpx_status (mirrors the reference hierarchy, types.hpp:17-45).
+struct Failure : std::runtime_error {
+  dcpx_status code;
+  Failure(dcpx_status c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+struct Instr {
+  int op = 0, division = 0, send = 0, peer = 0, dst = 0, count = 0;
+  int64_t offset = 0;
+  std::string tag;
+};
+
+struct PlanCopy {  // owned copy of one dcpx_plan_view
+  int device = 0, divisions = 0;
+  int cap[3] = {0, 0, 0};
+  std::vector<dcpx_block_slot> res_q, res_kv, res_o;
+  std::vector<Instr> ins;
+  std::vector<dcpx_attention_item> items;
+  std::vector<int32_t> srcs;
+  std::vector<dcpx_copy_item> copies;
+  std::vector<dcpx_block_slot> blocks;
+  std::vector<int32_t> rows;
+};
+
+struct GraphCopy {
+  int H = 0, G = 0, D = 0, bpe = 2;
+  std::vector<int64_t> seq_lengths, block_sizes, seq_offsets;
+  std::vector<int32_t> ranges;  // [T][4]
+  std::vector<dcpx_data_block> data_blocks;
+  std::vector<dcpx_comp_block> comp_blocks;
+  int64_t total_tokens() const { return seq_offsets.empty() ? 0 : seq_offsets.back(); }
+};
+
+// Device-resident job list helper (uploaded once at prepare).
+struct JobList {
+  DevJobs dj;
+  std::vector<void*> owned;
+};
+
+enum class OpKind { kFwdAttn, kMerge, kCopy, kCommLaunch, kCommWait, kNop };
+
+struct Op {
+  OpKind kind = OpKind::kNop;
+  int division = 0;
+  int instr = 0;
+  // kFwdAttn
+  FwdUnit* units = nullptr;
+  FwdStep* steps = nullptr;
+  ItemMask* items = nullptr;
+  int num_units = 0, grid = 0;
+  uint64_t flops = 0;
+  // kMerge / kCopy
+  JobList jobs;
+  int32_t* src_rows = nullptr;
+  // comm
+  int send = 0, peer = 0;
+  std::string tag;
+  std::vector<dcpx_block_slot> blocks;
+  uint64_t bytes = 0;
+};
+
+struct DevState {
+  int ordinal = 0;
+  cudaStream_t cs = nullptr, ms = nullptr;
+  int64_t slot_rows = 0;
+  int64_t cap_q = 0, cap_kv = 0, cap_o = 0;  // physical slots
+  std::vector<int32_t> o_phys;               // plan O slot -> physical slot
+  __nv_bfloat16 *q = nullptr, *kv = nullptr, *o = nullptr;
+  float* lse = nullptr;
+  int32_t* ranges = nullptr;
+  CUtensorMap tm_q{}, tm_kv{};
+  std::vector<Op> prog;
+  JobList scatter_q, scatter_k, scatter_v, gather_o, gather_lse;
+  std::vector<int32_t> final_o_slot;  // per resident_o entry: physical slot holding the result
+  std::vector<cudaEvent_t> events;
+  size_t next_event = 0;
+  cudaEvent_t t0 = nullptr, t1 = nullptr;
+  int launches = 0;
+};
+
+struct Options {
+  bool fuse_reductions = true;
+  bool remap_copies = true;
+  bool check_rows = false;
+  bool timing = true;
+};
+
+class Executor {
+ public:
+  Executor(int ndev, const int* ordinals);
+  ~Executor();
+  void prepare(int nplans, const dcpx_plan_view* plans, const dcpx_graph_view* g,
+               const dcpx_mask_view* m);
+  void load_inputs(const void* q, const void* k, const void* v, bool host);
+  void forward(void* o_out, float* lse_out, dcpx_report* rep, bool host);
+  void synchronize();
+  void debug_arena(int dev, int kind, void** ptr, int64_t* rows);
+  Options opt;
+  std::string last_error;
+
+ private:
+  void compile_device(int d);
+  void compile_attention(int d, int ins_index, std::vector<bool>& fused_red);
+  void build_io_jobs(int d);
+  void simulate_order();
+  cudaEvent_t event(int d);
+  void free_all();
+
+  int R_ = 0;
+  std::vector<int> ordinals_;
+  std::vector<PlanCopy> plans_;
+  GraphCopy g_;
+  std::vector<DevState> dev_;
+  // global issue order from the lockstep simulation: (device, op index)
+  std::vector<std::pair<int, int>> order_;
+  std::vector<void*> allocs_;  // (ordinal, ptr) freed in destructor
+  std::vector<int> alloc_dev_;
+  char* in_stage_ = nullptr;   // host-input staging on device 0 (load_inputs_host)
+  char* out_stage_ = nullptr;  // host-output staging on device 0 (forward_host)
+  bool prepared_ = false;
+  // report
+  std::vector<std::map<std::pair<int, int>, uint64_t>> comm_bytes_;
+  std::vector<std::vector<uint64_t>> comp_flops_;
+  void* alloc(int d, size_t bytes);
+  template <class T>
+  T* upload(int d, const std::vector<T>& v);
+  JobList make_jobs(int d, const std::vector<RowCopyJob>& jobs);
+  template <class J>
+  JobList make_row_jobs(int d, const std::vector<J>& jobs, const std::vector<int>& rows, int rows_per_block);
+};
+
+}  // namespace dcpx

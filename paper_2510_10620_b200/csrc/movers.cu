@@ -1,0 +1,185 @@
+// movers.cu — HBM-bound helpers of the executor:
+//  * row_copy   : batched strided row copies (resident scatter of packed Q/K/V, output
+//                 gather, CopyInstr, LOCAL-transport block transfers incl. peer reads).
+//  * merge      : K2, rescale-and-sum merge of (O, LSE) partials, the reference's
+//                 exec_reduction (simexec.hpp:80-111) in LSE form: partials with
+//                 LSE = -inf (l = 0) are skipped (:96-103), rows with no partial stay 0.
+//  * bwd helpers: Delta = rowsum(dO o O) preprocess, fp32 accumulate of returned
+//                 partial gradients, fp32 -> bf16 conversion.
+// All kernels use 16-byte vector accesses when the job is 16-byte aligned.
+#include <cuda_bf16.h>
+#include <math_constants.h>
+
+#include "movers.h"
+
+namespace dcpx {
+
+__global__ void row_copy_kernel(const RowCopyJob* __restrict__ jobs, const int32_t* __restrict__ job_of_block,
+                                const int32_t* __restrict__ first_chunk, int64_t src_adjust,
+                                int64_t dst_adjust) {
+  const int b = blockIdx.x;
+  const int j = job_of_block[b];
+  RowCopyJob J = jobs[j];
+  J.src += src_adjust;
+  J.dst += dst_adjust;
+  const int chunk = b - first_chunk[j];  // chunk of kRowsPerChunk rows
+  const int r0 = chunk * kRowsPerChunk;
+  const int r1 = min(J.rows, r0 + kRowsPerChunk);
+  const bool vec = ((reinterpret_cast<uintptr_t>(J.src) | reinterpret_cast<uintptr_t>(J.dst) |
+                     (uintptr_t)J.src_stride | (uintptr_t)J.dst_stride | (uintptr_t)J.row_bytes) & 15) == 0;
+  if (vec) {
+    const int per_row = J.row_bytes >> 4;
+    const int total = (r1 - r0) * per_row;
+    for (int i = threadIdx.x; i < total; i += blockDim.x) {
+      const int r = r0 + i / per_row, c = i % per_row;
+      const uint4* s = reinterpret_cast<const uint4*>(J.src + (int64_t)r * J.src_stride) + c;
+      uint4* d = reinterpret_cast<uint4*>(J.dst + (int64_t)r * J.dst_stride) + c;
+      *d = *s;
+    }
+  } else {
+    const int per_row = J.row_bytes >> 2;
+    const int total = (r1 - r0) * per_row;
+    for (int i = threadIdx.x; i < total; i += blockDim.x) {
+      const int r = r0 + i / per_row, c = i % per_row;
+      const uint32_t* s = reinterpret_cast<const uint32_t*>(J.src + (int64_t)r * J.src_stride) + c;
+      uint32_t* d = reinterpret_cast<uint32_t*>(J.dst + (int64_t)r * J.dst_stride) + c;
+      *d = *s;
+    }
+  }
+}
+
+// One warp per pair of rows: 16 lanes x 16 B cover one 128-wide bf16 row.
+__global__ void merge_kernel(const MergeJob* __restrict__ jobs, const int32_t* __restrict__ src_rows,
+                             const int32_t* __restrict__ job_of_block, const int32_t* __restrict__ first_chunk,
+                             __nv_bfloat16* o_arena, float* lse_arena) {
+  const int b = blockIdx.x;
+  const int j = job_of_block[b];
+  const MergeJob J = jobs[j];
+  const int row_in_job = (b - first_chunk[j]) * 16 + (threadIdx.x >> 4);  // 256 threads -> 16 rows
+  if (row_in_job >= J.n_rows) return;
+  const int sub = threadIdx.x & 15;
+  float lse[kMaxMergeSrcs];
+  float mx = -CUDART_INF_F;
+  for (int i = 0; i < J.n_src; ++i) {
+    lse[i] = lse_arena[(int64_t)src_rows[J.src_begin + i] + row_in_job];
+    mx = fmaxf(mx, lse[i]);
+  }
+  float acc[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) acc[e] = 0.f;
+  float lse_out = -CUDART_INF_F;
+  if (mx != -CUDART_INF_F) {
+    float denom = 0.f;
+    for (int i = 0; i < J.n_src; ++i) denom += lse[i] == -CUDART_INF_F ? 0.f : __expf(lse[i] - mx);
+    lse_out = mx + __logf(denom);
+    for (int i = 0; i < J.n_src; ++i) {
+      if (lse[i] == -CUDART_INF_F) continue;
+      const float w = __expf(lse[i] - mx) / denom;
+      const uint4 v = *(reinterpret_cast<const uint4*>(o_arena + ((int64_t)src_rows[J.src_begin + i] + row_in_job) * 128) + sub);
+      const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        acc[2 * e] = fmaf(w, __bfloat162float(h[e].x), acc[2 * e]);
+        acc[2 * e + 1] = fmaf(w, __bfloat162float(h[e].y), acc[2 * e + 1]);
+      }
+    }
+  }
+  __syncwarp();
+  uint4 out;
+  __nv_bfloat162* ho = reinterpret_cast<__nv_bfloat162*>(&out);
+#pragma unroll
+  for (int e = 0; e < 4; ++e) ho[e] = __floats2bfloat162_rn(acc[2 * e], acc[2 * e + 1]);
+  *(reinterpret_cast<uint4*>(o_arena + ((int64_t)J.dst_row0 + row_in_job) * 128) + sub) = out;
+  if (sub == 0) lse_arena[(int64_t)J.dst_row0 + row_in_job] = lse_out;
+}
+
+// Delta[row] = sum_d dO[row][d] * O[row][d] (fp32), one 16-lane group per row.
+__global__ void delta_kernel(const RowJob* __restrict__ jobs, const int32_t* __restrict__ job_of_block,
+                             const int32_t* __restrict__ first_chunk, const __nv_bfloat16* o_arena,
+                             const __nv_bfloat16* do_arena, float* delta) {
+  const int b = blockIdx.x;
+  const int j = job_of_block[b];
+  const RowJob J = jobs[j];
+  const int r = (b - first_chunk[j]) * 16 + (threadIdx.x >> 4);
+  const int sub = threadIdx.x & 15;
+  float s = 0.f;
+  if (r < J.rows) {
+    const uint4 a = *(reinterpret_cast<const uint4*>(o_arena + ((int64_t)J.a_row0 + r) * 128) + sub);
+    const uint4 d = *(reinterpret_cast<const uint4*>(do_arena + ((int64_t)J.b_row0 + r) * 128) + sub);
+    const __nv_bfloat162* ha = reinterpret_cast<const __nv_bfloat162*>(&a);
+    const __nv_bfloat162* hd = reinterpret_cast<const __nv_bfloat162*>(&d);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      s = fmaf(__bfloat162float(ha[e].x), __bfloat162float(hd[e].x), s);
+      s = fmaf(__bfloat162float(ha[e].y), __bfloat162float(hd[e].y), s);
+    }
+  }
+#pragma unroll
+  for (int o = 8; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (r < J.rows && sub == 0) delta[(int64_t)J.b_row0 + r] = s;
+}
+
+// dst_f32[row][c] += bf16 src[row][c] (returned partial gradients), rows of 128.
+__global__ void accum_bf16_kernel(const RowJob* __restrict__ jobs, const int32_t* __restrict__ job_of_block,
+                                  const int32_t* __restrict__ first_chunk, const __nv_bfloat16* src_base,
+                                  float* dst_base) {
+  const int b = blockIdx.x;
+  const int j = job_of_block[b];
+  const RowJob J = jobs[j];
+  const int r = (b - first_chunk[j]) * 16 + (threadIdx.x >> 4);
+  const int sub = threadIdx.x & 15;
+  if (r >= J.rows) return;
+  const uint4 a = *(reinterpret_cast<const uint4*>(src_base + ((int64_t)J.a_row0 + r) * 128) + sub);
+  const __nv_bfloat162* ha = reinterpret_cast<const __nv_bfloat162*>(&a);
+  float4* d = reinterpret_cast<float4*>(dst_base + ((int64_t)J.b_row0 + r) * 128) + 2 * sub;
+  float4 x = d[0], y = d[1];
+  x.x += __bfloat162float(ha[0].x); x.y += __bfloat162float(ha[0].y);
+  x.z += __bfloat162float(ha[1].x); x.w += __bfloat162float(ha[1].y);
+  y.x += __bfloat162float(ha[2].x); y.y += __bfloat162float(ha[2].y);
+  y.z += __bfloat162float(ha[3].x); y.w += __bfloat162float(ha[3].y);
+  d[0] = x;
+  d[1] = y;
+}
+
+// bf16 dst[b_row0 + r * b_stride] (element offsets) = fp32 src arena row a_row0 + r:
+// gradient output gather / wire staging.
+__global__ void f32_to_bf16_kernel(const RowJob* __restrict__ jobs, const int32_t* __restrict__ job_of_block,
+                                   const int32_t* __restrict__ first_chunk, const float* src_base,
+                                   __nv_bfloat16* dst_base) {
+  const int b = blockIdx.x;
+  const int j = job_of_block[b];
+  const RowJob J = jobs[j];
+  const int r = (b - first_chunk[j]) * 16 + (threadIdx.x >> 4);
+  const int sub = threadIdx.x & 15;
+  if (r >= J.rows) return;
+  const float4* s = reinterpret_cast<const float4*>(src_base + ((int64_t)J.a_row0 + r) * 128) + 2 * sub;
+  const float4 x = s[0], y = s[1];
+  uint4 out;
+  __nv_bfloat162* ho = reinterpret_cast<__nv_bfloat162*>(&out);
+  ho[0] = __floats2bfloat162_rn(x.x, x.y);
+  ho[1] = __floats2bfloat162_rn(x.z, x.w);
+  ho[2] = __floats2bfloat162_rn(y.x, y.y);
+  ho[3] = __floats2bfloat162_rn(y.z, y.w);
+  *(reinterpret_cast<uint4*>(dst_base + J.b_row0 + (int64_t)r * J.b_stride) + sub) = out;
+}
+
+// ---------------------------------------------------------------------------- launchers
+void launch_row_copy(const DevJobs& j, cudaStream_t s, int64_t src_adjust, int64_t dst_adjust) {
+  if (j.n_blocks)
+    row_copy_kernel<<<j.n_blocks, 256, 0, s>>>(static_cast<const RowCopyJob*>(j.jobs), j.job_of_block,
+                                               j.first_chunk, src_adjust, dst_adjust);
+}
+void launch_merge(const DevJobs& j, const int32_t* src_rows, __nv_bfloat16* o, float* lse, cudaStream_t s) {
+  if (j.n_blocks) merge_kernel<<<j.n_blocks, 256, 0, s>>>(static_cast<const MergeJob*>(j.jobs), src_rows, j.job_of_block, j.first_chunk, o, lse);
+}
+void launch_delta(const DevJobs& j, const __nv_bfloat16* o, const __nv_bfloat16* d_o, float* delta, cudaStream_t s) {
+  if (j.n_blocks) delta_kernel<<<j.n_blocks, 256, 0, s>>>(static_cast<const RowJob*>(j.jobs), j.job_of_block, j.first_chunk, o, d_o, delta);
+}
+void launch_accum(const DevJobs& j, const __nv_bfloat16* src, float* dst, cudaStream_t s) {
+  if (j.n_blocks) accum_bf16_kernel<<<j.n_blocks, 256, 0, s>>>(static_cast<const RowJob*>(j.jobs), j.job_of_block, j.first_chunk, src, dst);
+}
+void launch_to_bf16(const DevJobs& j, const float* src, __nv_bfloat16* dst, cudaStream_t s) {
+  if (j.n_blocks) f32_to_bf16_kernel<<<j.n_blocks, 256, 0, s>>>(static_cast<const RowJob*>(j.jobs), j.job_of_block, j.first_chunk, src, dst);
+}
+
+}  // namespace dcpx

@@ -1,0 +1,50 @@
+// movers.h — job descriptors + launchers of the HBM-bound helper kernels (movers.cu).
+#pragma once
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "program.h"
+
+namespace dcpx {
+
+constexpr int kRowsPerChunk = 64;
+constexpr int kMaxMergeSrcs = 64;
+
+// Strided row copy: rows x row_bytes from src (stride src_stride) to dst. The launch
+// adds src_adjust / dst_adjust to every job's pointers, so jobs built at prepare time
+// can hold offsets relative to caller buffers that are only known per call.
+struct RowCopyJob {
+  const char* src;
+  char* dst;
+  int64_t src_stride, dst_stride;
+  int32_t rows, row_bytes;
+};
+
+// Generic row job over 128-wide rows: a_row0 / b_row0 index rows of two arenas.
+struct RowJob {
+  int64_t a_row0, b_row0;
+  int64_t b_stride;  // f32_to_bf16 only: b_row0 is an element offset, rows b_stride apart
+  int32_t rows, _pad;
+};
+
+// A device-resident job list with its block decomposition (block -> job, chunk).
+struct DevJobs {
+  void* jobs = nullptr;              // RowCopyJob / MergeJob / RowJob array
+  int32_t* job_of_block = nullptr;
+  int32_t* first_chunk = nullptr;
+  int32_t n_blocks = 0;
+  int32_t n_jobs = 0;
+};
+
+void launch_row_copy(const DevJobs& j, cudaStream_t s, int64_t src_adjust = 0, int64_t dst_adjust = 0);
+void launch_merge(const DevJobs& j, const int32_t* src_rows, __nv_bfloat16* o, float* lse, cudaStream_t s);
+void launch_delta(const DevJobs& j, const __nv_bfloat16* o, const __nv_bfloat16* d_o, float* delta, cudaStream_t s);
+void launch_accum(const DevJobs& j, const __nv_bfloat16* src, float* dst, cudaStream_t s);
+void launch_to_bf16(const DevJobs& j, const float* src, __nv_bfloat16* dst, cudaStream_t s);
+
+void launch_attn_fwd(const CUtensorMap& tm_q, const CUtensorMap& tm_kv, const FwdParams& p, int grid,
+                     cudaStream_t stream);
+
+}  // namespace dcpx

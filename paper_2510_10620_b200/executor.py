@@ -1,0 +1,178 @@
+"""Python mirror of the DCP executor interface over the C ABI (include/dcpx.h).
+
+The paper's user-facing API is ``DCPExecutor(group).prepare(plan)`` plus
+``DCPAttn.apply(executor, q, kv)``; the reference's executor entry
+point is ``dcp::run(plans, g, payload, topo, opts) -> SimResult`` (simexec.hpp:207-209).
+This module exposes both shapes on top of ``libdcpx.so``:
+
+* :class:`DCPExecutor` — ``prepare(bundle)``, ``load_inputs(q, k, v)``, ``forward()``,
+  ``backward(d_o)`` on packed bf16 CUDA tensors (token-major ``[T, H, D]`` / ``[T, G, D]``).
+* :func:`run` — the reference-shaped convenience call returning outputs + report.
+
+There is no CPU fallback: importing works without a GPU, but every compute call goes
+through the sm_100a library and raises if it is missing or fails.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from typing import Optional, Sequence
+
+from . import plans as P
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libdcpx.so")
+
+STATUS = {0: "OK", 1: "Error", 2: "DeadlockError", 3: "TagMismatchError", 4: "BufferOverflowError",
+          5: "InfeasibleError", 6: "CudaError", 7: "Unsupported"}
+
+# Every symbol include/dcpx.h declares (checked by tests/test_capi_symbols.py).
+EXPORTS = ["dcpx_create", "dcpx_create_rank", "dcpx_nccl_unique_id", "dcpx_prepare",
+           "dcpx_load_inputs", "dcpx_load_inputs_host", "dcpx_forward", "dcpx_forward_host",
+           "dcpx_backward", "dcpx_backward_host", "dcpx_synchronize", "dcpx_debug_arena",
+           "dcpx_set_option", "dcpx_last_error", "dcpx_version", "dcpx_destroy"]
+
+
+class DCPXError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"{STATUS.get(code, code)}: {msg}")
+        self.code = code
+        self.kind = STATUS.get(code, str(code))
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"libdcpx.so not built ({LIB_PATH}); run __graft_entry__.build()")
+        L = C.CDLL(LIB_PATH)
+        L.dcpx_last_error.restype = C.c_char_p
+        L.dcpx_version.restype = C.c_char_p
+        for name in ("dcpx_create", "dcpx_create_rank", "dcpx_nccl_unique_id", "dcpx_prepare",
+                     "dcpx_load_inputs", "dcpx_load_inputs_host", "dcpx_forward",
+                     "dcpx_forward_host", "dcpx_backward", "dcpx_backward_host",
+                     "dcpx_synchronize", "dcpx_debug_arena", "dcpx_set_option"):
+            getattr(L, name).restype = C.c_int
+        L.dcpx_create.argtypes = [C.c_int, C.POINTER(C.c_int), C.c_int, C.POINTER(C.c_void_p)]
+        L.dcpx_create_rank.argtypes = [C.c_int, C.c_int, C.c_int, C.c_void_p, C.POINTER(C.c_void_p)]
+        L.dcpx_prepare.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p]
+        L.dcpx_load_inputs.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+        L.dcpx_load_inputs_host.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+        L.dcpx_forward.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+        L.dcpx_forward_host.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+        L.dcpx_backward.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                    C.c_void_p]
+        L.dcpx_backward_host.argtypes = L.dcpx_backward.argtypes
+        L.dcpx_synchronize.argtypes = [C.c_void_p]
+        L.dcpx_debug_arena.argtypes = [C.c_void_p, C.c_int, C.c_int, C.POINTER(C.c_void_p),
+                                       C.POINTER(C.c_int64)]
+        L.dcpx_set_option.argtypes = [C.c_void_p, C.c_char_p, C.c_int64]
+        L.dcpx_last_error.argtypes = [C.c_void_p]
+        L.dcpx_destroy.argtypes = [C.c_void_p]
+        L.dcpx_nccl_unique_id.argtypes = [C.c_void_p]
+        _lib = L
+    return _lib
+
+
+def _report_dict(r: P.c_report) -> dict:
+    n = r.devices
+    return dict(devices=n, stages=r.stages, total_bytes=int(r.total_bytes),
+                total_flops=int(r.total_flops), per_device_send=[int(x) for x in r.per_device_send[:n]],
+                per_device_recv=[int(x) for x in r.per_device_recv[:n]], wire_bytes=int(r.wire_bytes),
+                makespan=r.makespan, device_ms=r.device_ms, kernel_launches=r.kernel_launches)
+
+
+def _ptr(t) -> Optional[int]:
+    return None if t is None else t.data_ptr()
+
+
+class DCPExecutor:
+    """One context executing the plans of `bundle`.
+
+    devices: CUDA ordinals, one per plan device (LOCAL transport, one process). Several
+    plan devices may share one GPU (single-GPU emulation of an R-device plan). For one
+    process per GPU use ``rank``/``world``/``nccl_id`` (NCCL transport)."""
+
+    def __init__(self, devices: Optional[Sequence[int]] = None, rank: Optional[int] = None,
+                 world: Optional[int] = None, nccl_id: Optional[bytes] = None, cuda_ordinal: int = 0):
+        self._h = C.c_void_p()
+        self.rank = rank
+        if rank is not None:
+            buf = C.create_string_buffer(bytes(nccl_id), 128)
+            self._check(lib().dcpx_create_rank(rank, world, cuda_ordinal, buf, C.byref(self._h)), create=True)
+            self.ndev = 1
+        else:
+            devices = list(devices or [0])
+            arr = (C.c_int * len(devices))(*devices)
+            self._check(lib().dcpx_create(len(devices), arr, 0, C.byref(self._h)), create=True)
+            self.ndev = len(devices)
+        self.bundle: Optional[P.PlanBundle] = None
+        self._keep = None
+
+    def __del__(self):
+        self.close()
+
+    def close(self):
+        if getattr(self, "_h", None) and self._h.value:
+            lib().dcpx_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def _check(self, rc: int, create: bool = False):
+        if rc != 0:
+            msg = lib().dcpx_last_error(None if create else self._h).decode()
+            raise DCPXError(rc, msg)
+
+    def set_option(self, key: str, value: int):
+        self._check(lib().dcpx_set_option(self._h, key.encode(), int(value)))
+
+    # -- DCPExecutor.prepare(execution_plan)
+    def prepare(self, bundle: P.PlanBundle):
+        keep, g, m, pv = bundle.c_views()
+        self._check(lib().dcpx_prepare(self._h, len(pv), pv, C.byref(g), C.byref(m)))
+        self.bundle = bundle
+        self._keep = (keep, g, m, pv)
+
+    def load_inputs(self, q, k, v):
+        if q.is_cuda:
+            self._check(lib().dcpx_load_inputs(self._h, _ptr(q), _ptr(k), _ptr(v)))
+        else:
+            self._check(lib().dcpx_load_inputs_host(self._h, _ptr(q), _ptr(k), _ptr(v)))
+
+    def forward(self, o=None, lse=None, host: bool = False) -> dict:
+        rep = P.c_report()
+        fn = lib().dcpx_forward_host if host else lib().dcpx_forward
+        self._check(fn(self._h, _ptr(o), _ptr(lse), C.byref(rep)))
+        return _report_dict(rep)
+
+    def backward(self, d_o, dq, dk, dv, host: bool = False) -> dict:
+        rep = P.c_report()
+        fn = lib().dcpx_backward_host if host else lib().dcpx_backward
+        self._check(fn(self._h, _ptr(d_o), _ptr(dq), _ptr(dk), _ptr(dv), C.byref(rep)))
+        return _report_dict(rep)
+
+    def synchronize(self):
+        self._check(lib().dcpx_synchronize(self._h))
+
+    def arena(self, dev: int, kind: int):
+        ptr, rows = C.c_void_p(), C.c_int64()
+        self._check(lib().dcpx_debug_arena(self._h, dev, kind, C.byref(ptr), C.byref(rows)))
+        return ptr.value, rows.value
+
+
+def run(bundle: P.PlanBundle, q, k, v, devices: Optional[Sequence[int]] = None):
+    """Reference-shaped call (simexec.hpp:207): executes all plans of `bundle` on the
+    given CUDA devices and returns (o [T,H,D] bf16, lse [H,T] fp32, report)."""
+    import torch
+    ex = DCPExecutor(devices or [q.device.index or 0] * bundle.R)
+    ex.prepare(bundle)
+    ex.load_inputs(q, k, v)
+    T, H, D = bundle.total_tokens, bundle.H, bundle.D
+    o = torch.zeros((T, H, D), dtype=torch.bfloat16, device=q.device)
+    lse = torch.full((H, T), float("-inf"), dtype=torch.float32, device=q.device)
+    rep = ex.forward(o, lse)
+    ex.synchronize()
+    ex.close()
+    return o, lse, rep

@@ -1,0 +1,84 @@
+"""Builds every native artefact in-tree (they travel to the GPU box with gpurun).
+
+  paper_2510_10620_b200/libdcpx.so  : the product — sm_100a kernels + executor + C ABI
+  planner/_build/libdcpplanner.so   : caller-side reference planner shim (needs /root/reference)
+  oracle/_build/liboracle.so        : C restatement (test infrastructure)
+  oracle/_ref/libdcpref.so          : the reference executor (test infrastructure; needs /root/reference)
+
+Incremental: a target is rebuilt only when one of its sources is newer.
+"""
+from __future__ import annotations
+
+import glob
+import os
+import subprocess
+import sys
+
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+REF = "/root/reference/proj"
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+
+
+def _stale(target, sources):
+    if not os.path.exists(target):
+        return True
+    t = os.path.getmtime(target)
+    return any(os.path.getmtime(s) > t for s in sources)
+
+
+def _run(cmd, cwd=REPO):
+    print("+", " ".join(cmd), flush=True)
+    subprocess.check_call(cmd, cwd=cwd)
+
+
+def build_dcpx(force=False):
+    csrc = os.path.join(REPO, "paper_2510_10620_b200", "csrc")
+    srcs = sorted(glob.glob(os.path.join(csrc, "*.cu")))
+    deps = srcs + glob.glob(os.path.join(csrc, "*.h")) + glob.glob(os.path.join(csrc, "*.cuh")) + \
+        [os.path.join(REPO, "include", "dcpx.h")]
+    out = os.path.join(REPO, "paper_2510_10620_b200", "libdcpx.so")
+    if not force and not _stale(out, deps):
+        return out
+    objdir = os.path.join(REPO, "build", "obj")
+    os.makedirs(objdir, exist_ok=True)
+    objs = []
+    for s in srcs:
+        o = os.path.join(objdir, os.path.basename(s) + ".o")
+        if force or _stale(o, [s] + [d for d in deps if not d.endswith(".cu")]):
+            _run([NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
+                  "-Xptxas", "-warn-spills", "-c", s, "-o", o])
+        objs.append(o)
+    _run([NVCC, *ARCH, "-shared", "-o", out, *objs, "-lcudart"])
+    return out
+
+
+def build_planner(force=False):
+    src = os.path.join(REPO, "planner", "dcp_planner_capi.cpp")
+    out = os.path.join(REPO, "planner", "_build", "libdcpplanner.so")
+    if not os.path.isdir(os.path.join(REF, "include", "dcp")):
+        if not os.path.exists(out):
+            print("planner shim: reference sources absent and no prebuilt library", file=sys.stderr)
+        return out
+    if force or _stale(out, [src, os.path.join(REPO, "include", "dcpx.h")]):
+        os.makedirs(os.path.dirname(out), exist_ok=True)
+        _run(["g++", "-std=c++20", "-O3", "-fPIC", "-shared", f"-I{REF}/include", f"-I{REF}/tests",
+              src, "-o", out, "-pthread"])
+    return out
+
+
+def build_oracle(force=False):
+    args = ["make", "-s", "-f", os.path.join(REPO, "oracle", "Makefile")]
+    if force:
+        args.append("-B")
+    _run(args)
+
+
+def build_all(force=False):
+    build_planner(force)
+    build_oracle(force)
+    return build_dcpx(force)
+
+
+if __name__ == "__main__":
+    build_all(force="--force" in sys.argv)
