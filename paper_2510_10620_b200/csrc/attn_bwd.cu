@@ -1,0 +1,317 @@
+// attn_bwd.cu — K1b: blockwise masked attention backward for DCP AttentionItems on
+// sm_100a (tcgen05 + TMEM + TMA). No reference exists; the math is the
+// gradient of exec_attention (simexec.hpp:33-76):
+//   P = exp(s - LSE), dV = P^T dO, dP = dO V^T, Delta = rowsum(dO o O),
+//   dS = P o (dP - Delta), dQ = scale * dS K, dK = scale * dS^T Q.
+//
+// Work unit = one 128-row kv sub-tile of one KV slot; it streams every (item, 128-row
+// q tile) step of the division that touches it (all heads of the GQA group, all q tiles),
+// accumulating dK and dV in TMEM. dQ of each step is reduce-added (fp32) into the
+// q slot's dQ accumulator.
+//
+// CTA = 384 threads, persistent:
+//   warp 0      TMA producer: K, V per unit; Q, dO tiles + LSE/Delta rows per step (2 stages)
+//   warp 1      TMEM owner + tcgen05.mma issuer
+//   warps 4-7   P / dS: thread = kv row (TMEM lane); P^T -> TMEM, dS^T -> smem (SW128)
+//   warps 8-11  dQ drain (TMEM -> red.global.add.v4.f32) and the dK epilogue
+// TMEM: S^T [0,128) (P^T bf16 overwrites [0,64)), dP^T [128,256) (reused for dQ),
+//       dV [256,384), dK [384,512).
+#include <cuda_bf16.h>
+#include <math_constants.h>
+
+#include "program.h"
+#include "sm100.cuh"
+
+namespace dcpx {
+
+constexpr int kBwdThreads = 384;
+// K 32K | V 32K | Q[2] 64K | dO[2] 64K | dS 32K | LSE[2] 1K | Delta[2] 1K | barriers
+constexpr int kBwdSmemMain = 224 * 1024;
+constexpr int kBwdSmem = kBwdSmemMain + 2048 + 256;
+
+struct BwdBarriers {
+  uint64_t kv_full, kv_empty;
+  uint64_t q_full[2], q_empty[2];
+  uint64_t s_full, p_ready, dq_full, dq_empty, ds_free, acc_full, acc_empty;
+  uint32_t tmem_base;
+};
+
+__device__ __forceinline__ uint32_t bwd_cls(uint32_t c) { return c & 3u; }
+
+// fp32 vector reduce-add into global memory (accumulators are shared with other CTAs
+// and with peer devices' gradient returns, so every update is atomic).
+__device__ __forceinline__ void red_add_v4(float* dst, const uint32_t* v) {
+  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst), "f"(__uint_as_float(v[0])),
+               "f"(__uint_as_float(v[1])), "f"(__uint_as_float(v[2])), "f"(__uint_as_float(v[3]))
+               : "memory");
+}
+
+__global__ void __launch_bounds__(kBwdThreads, 1)
+    attn_bwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_do,
+                    const __grid_constant__ CUtensorMap tm_kv, const BwdParams p) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint8_t* sK = smem;
+  uint8_t* sV = smem + 32768;
+  uint8_t* sQ = smem + 65536;     // [2 stages][32 KiB]
+  uint8_t* sDO = smem + 131072;   // [2 stages][32 KiB]
+  uint8_t* sDS = smem + 196608;   // dS^T [kv rows][q], two q halves of 16 KiB, SW128
+  float* sLSE = reinterpret_cast<float*>(smem + kBwdSmemMain);          // [2][128] (log2 units)
+  float* sDelta = reinterpret_cast<float*>(smem + kBwdSmemMain + 1024);  // [2][128]
+  BwdBarriers& bars = *reinterpret_cast<BwdBarriers*>(smem + kBwdSmemMain + 2048);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  if ((smem_u32(smem) & 1023u) != 0) __trap();  // SW128 operands need 1 KiB alignment
+
+  if (threadIdx.x == 0) {
+    mbar_init(&bars.kv_full, 1);
+    mbar_init(&bars.kv_empty, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&bars.q_full[i], 1);
+      mbar_init(&bars.q_empty[i], 1);
+    }
+    mbar_init(&bars.s_full, 1);
+    mbar_init(&bars.p_ready, 128);
+    mbar_init(&bars.dq_full, 1);
+    mbar_init(&bars.dq_empty, 128);
+    mbar_init(&bars.ds_free, 1);
+    mbar_init(&bars.acc_full, 1);
+    mbar_init(&bars.acc_empty, 256);
+    fence_barrier_init();
+    tma_prefetch_desc(&tm_q);
+    tma_prefetch_desc(&tm_do);
+    tma_prefetch_desc(&tm_kv);
+  }
+  if (warp == 1) tmem_alloc<512>(&bars.tmem_base);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = bars.tmem_base;
+  if (warp < 4) asm volatile("setmaxnreg.dec.sync.aligned.u32 88;");
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ producer
+    if (lane == 0) {
+      uint32_t g = 0, it = 0;
+      for (int u = blockIdx.x; u < p.num_units; u += gridDim.x, ++it) {
+        const BwdUnit U = p.units[u];
+        mbar_wait(&bars.kv_empty, (it & 1) ^ 1);
+        mbar_arrive_expect_tx(&bars.kv_full, 65536);
+        for (int h = 0; h < 2; ++h) {
+          tma_load_2d(&tm_kv, &bars.kv_full, sK + h * 16384, 64 * h, U.kv_row0);
+          tma_load_2d(&tm_kv, &bars.kv_full, sV + h * 16384, 64 * h, U.kv_row0 + p.slot_rows);
+        }
+        for (int j = 0; j < U.step_count; ++j, ++g) {
+          const BwdStep S = p.steps[U.step_begin + j];
+          const int st = g & 1;
+          mbar_wait(&bars.q_empty[st], ((g >> 1) & 1) ^ 1);
+          mbar_arrive_expect_tx(&bars.q_full[st], 65536 + 1024);
+          for (int h = 0; h < 2; ++h) {
+            tma_load_2d(&tm_q, &bars.q_full[st], sQ + st * 32768 + h * 16384, 64 * h, S.q_row0);
+            tma_load_2d(&tm_do, &bars.q_full[st], sDO + st * 32768 + h * 16384, 64 * h, S.q_row0);
+          }
+          bulk_load(sLSE + st * 128, p.lse2 + S.q_row0, 512, &bars.q_full[st]);
+          bulk_load(sDelta + st * 128, p.delta + S.q_row0, 512, &bars.q_full[st]);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    if (lane == 0) {
+      const uint32_t id_kmaj = idesc_bf16_f32(128, 128, 0, 0);   // A K-major, B K-major
+      const uint32_t id_bmn = idesc_bf16_f32(128, 128, 0, 1);    // A K-major, B MN-major
+      const uint32_t id_abmn = idesc_bf16_f32(128, 128, 1, 1);   // A MN-major, B MN-major
+      const uint32_t sk = smem_u32(sK), sv = smem_u32(sV), sq = smem_u32(sQ), sdo = smem_u32(sDO),
+                     sds = smem_u32(sDS);
+      uint32_t g = 0, it = 0;
+      for (int u = blockIdx.x; u < p.num_units; u += gridDim.x, ++it) {
+        const BwdUnit U = p.units[u];
+        mbar_wait(&bars.kv_full, it & 1);
+        tc_fence_after();
+        for (int j = 0; j < U.step_count; ++j, ++g) {
+          const int st = g & 1;
+          mbar_wait(&bars.q_full[st], (g >> 1) & 1);
+          tc_fence_after();
+          // S^T = K Q^T  -> cols [0,128)
+          for (int kk = 0; kk < 8; ++kk) {
+            const uint32_t off = (kk >> 2) * 16384 + (kk & 3) * 32;
+            umma_ss(tbase, sdesc_sw128(sk + off, 16, 1024), sdesc_sw128(sq + st * 32768 + off, 16, 1024),
+                    id_kmaj, kk > 0);
+          }
+          // dP^T = V dO^T -> cols [128,256) once the previous dQ has been drained
+          if (g > 0) {
+            mbar_wait(&bars.dq_empty, (g - 1) & 1);
+            tc_fence_after();
+          }
+          for (int kk = 0; kk < 8; ++kk) {
+            const uint32_t off = (kk >> 2) * 16384 + (kk & 3) * 32;
+            umma_ss(tbase + 128, sdesc_sw128(sv + off, 16, 1024), sdesc_sw128(sdo + st * 32768 + off, 16, 1024),
+                    id_kmaj, kk > 0);
+          }
+          umma_commit(&bars.s_full);
+          mbar_wait(&bars.p_ready, g & 1);
+          tc_fence_after();
+          if (j == 0) {
+            mbar_wait(&bars.acc_empty, (it & 1) ^ 1);
+            tc_fence_after();
+          }
+          // dV += P^T dO   (A = P^T in TMEM, B = dO MN-major)
+          for (int kk = 0; kk < 8; ++kk)
+            umma_ts(tbase + 256, tbase + kk * 8, sdesc_sw128(sdo + st * 32768 + kk * 2048, 16384, 1024), id_bmn,
+                    (j > 0 || kk > 0) ? 1u : 0u);
+          // dK += dS^T Q   (A = dS^T K-major in smem, B = Q MN-major)
+          for (int kk = 0; kk < 8; ++kk) {
+            const uint32_t off = (kk >> 2) * 16384 + (kk & 3) * 32;
+            umma_ss(tbase + 384, sdesc_sw128(sds + off, 16, 1024),
+                    sdesc_sw128(sq + st * 32768 + kk * 2048, 16384, 1024), id_bmn, (j > 0 || kk > 0) ? 1u : 0u);
+          }
+          umma_commit(&bars.q_empty[st]);
+          // dQ = dS K      (A = dS MN-major in smem, B = K MN-major) -> cols [128,256)
+          for (int kk = 0; kk < 8; ++kk)
+            umma_ss(tbase + 128, sdesc_sw128(sds + kk * 2048, 16384, 1024), sdesc_sw128(sk + kk * 2048, 16384, 1024),
+                    id_abmn, kk > 0);
+          umma_commit(&bars.dq_full);
+          umma_commit(&bars.ds_free);
+        }
+        umma_commit(&bars.acc_full);
+        umma_commit(&bars.kv_empty);
+      }
+    }
+  } else if (warp >= 4 && warp < 8) {
+    // ------------------------------------------------------------ P / dS (thread = kv row)
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 208;");
+    const int j = ((warp & 3) << 5) + lane;
+    const uint32_t lane_addr = tbase + ((uint32_t)((warp & 3) * 32) << 16);
+    uint32_t g = 0, it = 0;
+    for (int u = blockIdx.x; u < p.num_units; u += gridDim.x, ++it) {
+      const BwdUnit U = p.units[u];
+      const bool kv_valid = j < U.n_kv;
+      for (int s = 0; s < U.step_count; ++s, ++g) {
+        const BwdStep S = p.steps[U.step_begin + s];
+        const int st = g & 1;
+        const uint32_t cl = bwd_cls(S.cls);
+        const ItemMask im = p.items[S.item];
+        const int64_t kvrel = (int64_t)S.col0 + j + im.kv_shift;  // in range coordinates
+        mbar_wait(&bars.s_full, g & 1);
+        tc_fence_after();
+        if (g > 0) mbar_wait(&bars.ds_free, (g - 1) & 1);
+        const float* lse2 = sLSE + st * 128;
+        const float* dlt = sDelta + st * 128;
+#pragma unroll 1
+        for (int c = 0; c < 128; c += 32) {
+          uint32_t sr[32], dr[32];
+          tmem_ld32(lane_addr + c, sr);
+          tmem_ld32(lane_addr + 128 + c, dr);
+          tmem_wait_ld();
+          uint32_t pk[16], dk[16];
+#pragma unroll
+          for (int e = 0; e < 16; ++e) {
+            float pv[2], dv[2];
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const int i = c + 2 * e + h;
+              bool ok = kv_valid && i < S.n_q;
+              if (ok && cl == kTilePartial) {
+                const int4 rg = __ldg(reinterpret_cast<const int4*>(p.ranges) + im.range_row0 + S.q_local0 + i);
+                ok = (kvrel >= rg.x && kvrel < rg.y) || (kvrel >= rg.z && kvrel < rg.w);
+              }
+              const float pe = ok ? fast_exp2(fmaf(__uint_as_float(sr[2 * e + h]), p.scale_log2, -lse2[i])) : 0.f;
+              pv[h] = pe;
+              dv[h] = pe * (__uint_as_float(dr[2 * e + h]) - dlt[i]) * p.scale;
+            }
+            pk[e] = pack_bf16(pv[0], pv[1]);
+            dk[e] = pack_bf16(dv[0], dv[1]);
+          }
+          tmem_st16(lane_addr + (c >> 1), pk);
+          // dS^T row j, q columns [c, c+32): 4 chunks of 16 B, 128B-swizzled
+          uint8_t* row = sDS + (c >> 6) * 16384 + j * 128;
+#pragma unroll
+          for (int q4 = 0; q4 < 4; ++q4) {
+            const int chunk = ((c & 63) >> 3) + q4;
+            *reinterpret_cast<uint4*>(row + ((chunk ^ (j & 7)) << 4)) =
+                make_uint4(dk[4 * q4], dk[4 * q4 + 1], dk[4 * q4 + 2], dk[4 * q4 + 3]);
+          }
+        }
+        tmem_wait_st();
+        fence_proxy_async_smem();
+        tc_fence_before();
+        mbar_arrive(&bars.p_ready);
+      }
+      // dV epilogue: dV acc [256,384) -> dKV accumulator (fp32, V half of the slot)
+      mbar_wait(&bars.acc_full, it & 1);
+      tc_fence_after();
+      float* dst = p.dkv_acc + ((int64_t)U.kv_row0 + p.slot_rows + j) * 128;
+#pragma unroll 1
+      for (int c = 0; c < 128; c += 32) {
+        uint32_t r[32];
+        tmem_ld32(lane_addr + 256 + c, r);
+        tmem_wait_ld();
+        if (kv_valid) {
+#pragma unroll
+          for (int e = 0; e < 32; e += 4) red_add_v4(dst + c + e, r + e);
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&bars.acc_empty);
+    }
+  } else if (warp >= 8) {
+    // ------------------------------------------------------------ dQ drain + dK epilogue
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 208;");
+    const int r = ((warp & 3) << 5) + lane;  // q row of the step / kv row of the unit
+    const uint32_t lane_addr = tbase + ((uint32_t)((warp & 3) * 32) << 16);
+    uint32_t g = 0, it = 0;
+    for (int u = blockIdx.x; u < p.num_units; u += gridDim.x, ++it) {
+      const BwdUnit U = p.units[u];
+      for (int s = 0; s < U.step_count; ++s, ++g) {
+        const BwdStep S = p.steps[U.step_begin + s];
+        mbar_wait(&bars.dq_full, g & 1);
+        tc_fence_after();
+        float* dst = p.dq_acc + ((int64_t)S.q_row0 + r) * 128;
+        const bool ok = r < S.n_q;
+#pragma unroll 1
+        for (int c = 0; c < 128; c += 32) {
+          uint32_t v[32];
+          tmem_ld32(lane_addr + 128 + c, v);
+          tmem_wait_ld();
+          if (ok) {
+#pragma unroll
+            for (int e = 0; e < 32; e += 4) red_add_v4(dst + c + e, v + e);
+          }
+        }
+        tc_fence_before();
+        mbar_arrive(&bars.dq_empty);
+      }
+      mbar_wait(&bars.acc_full, it & 1);
+      tc_fence_after();
+      float* dst = p.dkv_acc + ((int64_t)U.kv_row0 + r) * 128;
+      const bool kv_valid = r < U.n_kv;
+#pragma unroll 1
+      for (int c = 0; c < 128; c += 32) {
+        uint32_t v[32];
+        tmem_ld32(lane_addr + 384 + c, v);
+        tmem_wait_ld();
+        if (kv_valid) {
+#pragma unroll
+          for (int e = 0; e < 32; e += 4) red_add_v4(dst + c + e, v + e);
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&bars.acc_empty);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc<512>(tbase);
+}
+
+void launch_attn_bwd(const CUtensorMap& tm_q, const CUtensorMap& tm_do, const CUtensorMap& tm_kv,
+                     const BwdParams& p, int grid, cudaStream_t stream) {
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(attn_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kBwdSmem);
+    configured = true;
+  }
+  attn_bwd_kernel<<<grid, kBwdThreads, kBwdSmem, stream>>>(tm_q, tm_do, tm_kv, p);
+}
+
+}  // namespace dcpx

@@ -111,7 +111,7 @@ void dcpx_destroy(dcpx_ctx* ctx) {
 
 }  // extern "C"
 
-// ---- entry points implemented in later milestones (backward, NCCL transport) -----------
+// ---- backward; NCCL transport entry points (implemented in nccl.cu once built) -----------
 extern "C" {
 dcpx_status dcpx_create_rank(int, int, int, const void*, dcpx_ctx** out) {
   if (out) *out = nullptr;
@@ -119,12 +119,10 @@ dcpx_status dcpx_create_rank(int, int, int, const void*, dcpx_ctx** out) {
   return DCPX_UNSUPPORTED;
 }
 dcpx_status dcpx_nccl_unique_id(void*) { return DCPX_UNSUPPORTED; }
-dcpx_status dcpx_backward(dcpx_ctx* ctx, const void*, void*, void*, void*, dcpx_report*) {
-  if (ctx) ctx->err = "backward not built yet";
-  return DCPX_UNSUPPORTED;
+dcpx_status dcpx_backward(dcpx_ctx* ctx, const void* d_o, void* dq, void* dk, void* dv, dcpx_report* rep) {
+  return guarded(ctx, [&](dcpx::Executor& ex) { ex.backward(d_o, dq, dk, dv, rep, false); });
 }
-dcpx_status dcpx_backward_host(dcpx_ctx* ctx, const void*, void*, void*, void*, dcpx_report*) {
-  if (ctx) ctx->err = "backward not built yet";
-  return DCPX_UNSUPPORTED;
+dcpx_status dcpx_backward_host(dcpx_ctx* ctx, const void* d_o, void* dq, void* dk, void* dv, dcpx_report* rep) {
+  return guarded(ctx, [&](dcpx::Executor& ex) { ex.backward(d_o, dq, dk, dv, rep, true); });
 }
 }

@@ -203,7 +203,8 @@ void Executor::prepare(int nplans, const dcpx_plan_view* plans, const dcpx_graph
                        const dcpx_mask_view* mv) {
   if (nplans != R_) throw Failure(DCPX_ERROR, "run: plan count does not match topology");  // simexec.hpp:211
   free_all();
-  in_stage_ = out_stage_ = nullptr;
+  in_stage_ = out_stage_ = bwd_stage_ = nullptr;
+  fwd_done_ = false;
   for (auto& d : dev_) {
     d.prog.clear();
     d.o_phys.clear();
@@ -427,6 +428,7 @@ void Executor::prepare(int nplans, const dcpx_plan_view* plans, const dcpx_graph
     }
     build_io_jobs(d);
   }
+  build_bwd_jobs();
   for (int d = 0; d < R_; ++d) {
     DeviceGuard g(dev_[d].ordinal);
     CUDA_OK(cudaDeviceSynchronize());
@@ -672,6 +674,18 @@ void Executor::compile_device(int d) {
     CUDA_OK(cudaMemset(D.kv, 0, std::max<int64_t>(1, D.cap_kv) * 2 * SR * 256));
     CUDA_OK(cudaMemset(D.o, 0, std::max<int64_t>(1, D.cap_o) * SR * 256));
     CUDA_OK(cudaMemset(D.lse, 0, std::max<int64_t>(1, D.cap_o) * SR * 4));
+    // backward arenas, parallel to the Q arena (dO, LSE*log2e, Delta, dQ accumulator)
+    // and to the KV arena (dK / dV accumulators)
+    const int64_t nq = std::max<int64_t>(1, D.cap_q), nkv = std::max<int64_t>(1, D.cap_kv);
+    D.d_o = static_cast<__nv_bfloat16*>(alloc(d, nq * SR * 256));
+    D.lse2 = static_cast<float*>(alloc(d, nq * SR * 4));
+    D.delta = static_cast<float*>(alloc(d, nq * SR * 4));
+    D.dq_acc = static_cast<float*>(alloc(d, nq * SR * 512));
+    D.dkv_acc = static_cast<float*>(alloc(d, nkv * 2 * SR * 512));
+    CUDA_OK(cudaMemset(D.d_o, 0, nq * SR * 256));
+    CUDA_OK(cudaMemset(D.lse2, 0, nq * SR * 4));
+    CUDA_OK(cudaMemset(D.delta, 0, nq * SR * 4));
+    D.tm_do = make_tmap(D.d_o, nq * SR);
     D.tm_q = make_tmap(D.q, std::max<int64_t>(1, D.cap_q) * SR);
     D.tm_kv = make_tmap(D.kv, std::max<int64_t>(1, D.cap_kv) * 2 * SR);
     std::vector<int32_t> ranges = g_.ranges;
@@ -690,68 +704,71 @@ void Executor::compile_device(int d) {
     switch (I.op) {
       case DCPX_OP_ATTENTION: {
         op.kind = OpKind::kFwdAttn;
+        // -- classify every item once: [128-row q tile][128-col kv sub-tile] -> empty /
+        //    partial / full, from the item rows (plan.hpp:231-242 or explicit rows)
+        struct ItemCls { int nks = 0, n_qt = 0, mask = 0; std::vector<uint8_t> cls; };
+        std::map<int, ItemCls> icl;
+        std::vector<ItemMask> masks;
+        for (int k = 0; k < I.count; ++k) {
+          const int idx = static_cast<int>(I.offset) + k;
+          const auto& it = P.items[idx];
+          const int n_q = static_cast<int>(it.q_end - it.q_begin);
+          const int n_k = static_cast<int>(it.kv_end - it.kv_begin);
+          ItemCls c;
+          c.nks = (n_k + 127) / 128;
+          c.n_qt = (n_q + 127) / 128;
+          ItemMask im{};
+          im.n_k = n_k;
+          const int32_t* rg;
+          if (it.rows_offset >= 0) {
+            im.range_row0 = TT + it.rows_offset;
+            im.kv_shift = 0;
+            rg = P.rows.data() + 4 * it.rows_offset;
+          } else {
+            im.range_row0 = g_.seq_offsets[it.seq] + it.q_begin;
+            im.kv_shift = it.kv_begin;
+            rg = g_.ranges.data() + 4 * (g_.seq_offsets[it.seq] + it.q_begin);
+          }
+          c.mask = static_cast<int>(masks.size());
+          masks.push_back(im);
+          std::vector<uint8_t> all_full(static_cast<size_t>(c.n_qt) * c.nks, 1), any(static_cast<size_t>(c.n_qt) * c.nks, 0);
+          uint64_t pairs = 0;
+          for (int r = 0; r < n_q; ++r) {
+            RelRange rr;
+            const int64_t sh = im.kv_shift;
+            rr.b0 = static_cast<int32_t>(std::max<int64_t>(rg[4 * r] - sh, 0));
+            rr.e0 = static_cast<int32_t>(std::min<int64_t>(rg[4 * r + 1] - sh, n_k));
+            rr.b1 = static_cast<int32_t>(std::max<int64_t>(rg[4 * r + 2] - sh, 0));
+            rr.e1 = static_cast<int32_t>(std::min<int64_t>(rg[4 * r + 3] - sh, n_k));
+            if (it.rows_offset >= 0 && (rg[4 * r] < 0 || rg[4 * r + 1] > n_k || rg[4 * r + 2] < 0 || rg[4 * r + 3] > n_k) &&
+                (rg[4 * r + 1] > rg[4 * r] || rg[4 * r + 3] > rg[4 * r + 2]))
+              throw Failure(DCPX_ERROR, "exec_attention: range outside kv tile");  // simexec.hpp:53
+            if (rr.e0 > rr.b0) pairs += rr.e0 - rr.b0;
+            if (rr.e1 > rr.b1) pairs += rr.e1 - rr.b1;
+            const int qt = r / 128;
+            for (int ks = 0; ks < c.nks; ++ks) {
+              const int c0 = ks * 128, c1 = std::min(n_k, c0 + 128);
+              const bool full = (c1 - c0 == 128) && ((rr.b0 <= c0 && rr.e0 >= c1) || (rr.b1 <= c0 && rr.e1 >= c1));
+              const bool hit = (rr.e0 > rr.b0 && rr.b0 < c1 && rr.e0 > c0) || (rr.e1 > rr.b1 && rr.b1 < c1 && rr.e1 > c0);
+              if (!full) all_full[qt * c.nks + ks] = 0;
+              if (hit) any[qt * c.nks + ks] = 1;
+            }
+          }
+          op.flops += 4ull * pairs * static_cast<uint64_t>(g_.D);
+          c.cls.resize(static_cast<size_t>(c.n_qt) * c.nks);
+          for (size_t q = 0; q < c.cls.size(); ++q)
+            c.cls[q] = !any[q] ? kTileEmpty : (all_full[q] ? kTileFull : kTilePartial);
+          icl[idx] = std::move(c);
+        }
+        // -- forward units: one per (group, pair of 128-row q tiles)
         std::vector<FwdUnit> units;
         std::vector<FwdStep> steps;
-        std::vector<ItemMask> masks;
         std::vector<int64_t> unit_cost;
-        std::map<int, int> mask_of_item;
         for (const auto& grp : groups_of[i]) {
           const auto& i0 = P.items[grp.items[0]];
           const int n_q = static_cast<int>(i0.q_end - i0.q_begin);
           const int n_pairs = (n_q + 255) / 256;
           const int n_qt = (n_q + 127) / 128;
-          // per item: classification table [q tile][kv sub-tile]
-          struct ItemCls { int nks; std::vector<uint8_t> cls; int mask; };
-          std::vector<ItemCls> ic;
-          for (int idx : grp.items) {
-            const auto& it = P.items[idx];
-            const int n_k = static_cast<int>(it.kv_end - it.kv_begin);
-            const int nks = (n_k + 127) / 128;
-            ItemMask im{};
-            im.n_k = n_k;
-            const int32_t* rg;
-            if (it.rows_offset >= 0) {
-              im.range_row0 = TT + it.rows_offset;
-              im.kv_shift = 0;
-              rg = P.rows.data() + 4 * it.rows_offset;
-            } else {
-              im.range_row0 = g_.seq_offsets[it.seq] + it.q_begin;
-              im.kv_shift = it.kv_begin;
-              rg = g_.ranges.data() + 4 * (g_.seq_offsets[it.seq] + it.q_begin);
-            }
-            ItemCls c;
-            c.nks = nks;
-            c.mask = static_cast<int>(masks.size());
-            masks.push_back(im);
-            std::vector<uint8_t> all_full(static_cast<size_t>(n_qt) * nks, 1), any(static_cast<size_t>(n_qt) * nks, 0);
-            uint64_t pairs = 0;
-            for (int r = 0; r < n_q; ++r) {
-              RelRange rr;
-              const int64_t sh = im.kv_shift;
-              rr.b0 = static_cast<int32_t>(std::max<int64_t>(rg[4 * r] - sh, 0));
-              rr.e0 = static_cast<int32_t>(std::min<int64_t>(rg[4 * r + 1] - sh, n_k));
-              rr.b1 = static_cast<int32_t>(std::max<int64_t>(rg[4 * r + 2] - sh, 0));
-              rr.e1 = static_cast<int32_t>(std::min<int64_t>(rg[4 * r + 3] - sh, n_k));
-              if (it.rows_offset >= 0 && (rg[4 * r] < 0 || rg[4 * r + 1] > n_k || rg[4 * r + 2] < 0 || rg[4 * r + 3] > n_k) &&
-                  (rg[4 * r + 1] > rg[4 * r] || rg[4 * r + 3] > rg[4 * r + 2]))
-                throw Failure(DCPX_ERROR, "exec_attention: range outside kv tile");  // simexec.hpp:53
-              if (rr.e0 > rr.b0) pairs += rr.e0 - rr.b0;
-              if (rr.e1 > rr.b1) pairs += rr.e1 - rr.b1;
-              const int qt = r / 128;
-              for (int ks = 0; ks < nks; ++ks) {
-                const int c0 = ks * 128, c1 = std::min(n_k, c0 + 128);
-                const bool full = (c1 - c0 == 128) && ((rr.b0 <= c0 && rr.e0 >= c1) || (rr.b1 <= c0 && rr.e1 >= c1));
-                const bool hit = (rr.e0 > rr.b0 && rr.b0 < c1 && rr.e0 > c0) || (rr.e1 > rr.b1 && rr.b1 < c1 && rr.e1 > c0);
-                if (!full) all_full[qt * nks + ks] = 0;
-                if (hit) any[qt * nks + ks] = 1;
-              }
-            }
-            op.flops += 4ull * pairs * static_cast<uint64_t>(g_.D);
-            c.cls.resize(static_cast<size_t>(n_qt) * nks);
-            for (size_t k = 0; k < c.cls.size(); ++k)
-              c.cls[k] = !any[k] ? kTileEmpty : (all_full[k] ? kTileFull : kTilePartial);
-            ic.push_back(std::move(c));
-          }
           for (int pr = 0; pr < n_pairs; ++pr) {
             FwdUnit U{};
             U.q_row0 = static_cast<int32_t>(i0.q_slot * SR + 256 * pr);
@@ -761,9 +778,9 @@ void Executor::compile_device(int d) {
             U.q_local0 = 256 * pr;
             U.step_begin = static_cast<int32_t>(steps.size());
             int64_t cost = 0;
-            for (size_t gi = 0; gi < grp.items.size(); ++gi) {
-              const auto& it = P.items[grp.items[gi]];
-              const auto& c = ic[gi];
+            for (int idx : grp.items) {
+              const auto& it = P.items[idx];
+              const auto& c = icl.at(idx);
               for (int ks = 0; ks < c.nks; ++ks) {
                 const uint32_t c0 = c.cls[(2 * pr) * c.nks + ks];
                 const uint32_t c1 = (2 * pr + 1 < n_qt) ? c.cls[(2 * pr + 1) * c.nks + ks] : kTileEmpty;
@@ -793,6 +810,56 @@ void Executor::compile_device(int d) {
         op.items = upload(d, masks);
         op.num_units = static_cast<int>(sorted.size());
         op.grid = std::min(op.num_units, num_sms(D.ordinal));
+        // -- backward units: one per (kv slot, 128-row kv sub-tile), streaming every
+        //    (item, q tile) of this instruction that reads it
+        std::map<int, std::vector<int>> by_kv;
+        for (int k = 0; k < I.count; ++k) by_kv[P.items[I.offset + k].kv_slot].push_back(static_cast<int>(I.offset) + k);
+        std::vector<BwdUnit> bunits;
+        std::vector<BwdStep> bsteps;
+        std::vector<int64_t> bcost;
+        for (const auto& [kv_slot, idxs] : by_kv) {
+          const auto& f = P.items[idxs[0]];
+          const int n_k = static_cast<int>(f.kv_end - f.kv_begin);
+          const int nks = (n_k + 127) / 128;
+          for (int ks = 0; ks < nks; ++ks) {
+            BwdUnit U{};
+            U.kv_row0 = static_cast<int32_t>(2 * kv_slot * SR + 128 * ks);
+            U.n_kv = std::min(128, n_k - 128 * ks);
+            U.step_begin = static_cast<int32_t>(bsteps.size());
+            for (int idx : idxs) {
+              const auto& it = P.items[idx];
+              if (it.kv_end - it.kv_begin != n_k) throw Failure(DCPX_ERROR, "kv slot read with two sizes in one instruction");
+              const auto& c = icl.at(idx);
+              const int n_q = static_cast<int>(it.q_end - it.q_begin);
+              for (int qt = 0; qt < c.n_qt; ++qt) {
+                const uint32_t cl = c.cls[qt * c.nks + ks];
+                if (!cl) continue;
+                BwdStep S{};
+                S.q_row0 = static_cast<int32_t>(it.q_slot * SR + 128 * qt);
+                S.n_q = std::min(128, n_q - 128 * qt);
+                S.item = c.mask;
+                S.q_local0 = 128 * qt;
+                S.col0 = 128 * ks;
+                S.cls = cl;
+                bsteps.push_back(S);
+              }
+            }
+            U.step_count = static_cast<int32_t>(bsteps.size()) - U.step_begin;
+            if (U.step_count == 0) continue;
+            bunits.push_back(U);
+            bcost.push_back(U.step_count);
+          }
+        }
+        std::vector<size_t> border(bunits.size());
+        std::iota(border.begin(), border.end(), 0);
+        std::stable_sort(border.begin(), border.end(), [&](size_t a, size_t b) { return bcost[a] > bcost[b]; });
+        std::vector<BwdUnit> bsorted;
+        for (size_t k : border) bsorted.push_back(bunits[k]);
+        op.bunits = upload(d, bsorted);
+        op.bsteps = upload(d, bsteps);
+        op.bitems = op.items;
+        op.bnum_units = static_cast<int>(bsorted.size());
+        op.bgrid = std::min(op.bnum_units, num_sms(D.ordinal));
         if (I.division >= 0 && I.division < static_cast<int>(comp_flops_.size())) comp_flops_[I.division][d] += op.flops;
         break;
       }
@@ -895,6 +962,141 @@ void Executor::build_io_jobs(int d) {
   D.scatter_v = make_jobs(d, sv);
   D.gather_o = make_jobs(d, go);
   D.gather_lse = make_jobs(d, gl);
+}
+
+void Executor::build_bwd_jobs() {
+  const int T = R_ ? plans_[0].divisions : 0;
+  const int64_t TT = g_.total_tokens(), H = g_.H, G = g_.G;
+  bwd_send_.assign(static_cast<size_t>(R_), 0);
+  bwd_recv_.assign(static_cast<size_t>(R_), 0);
+  std::map<int, std::pair<int, int>> owner;  // resident Q / KV block -> (device, slot)
+  for (int d = 0; d < R_; ++d) {
+    for (const auto& r : plans_[d].res_q) owner[r.block] = {d, r.slot};
+    for (const auto& r : plans_[d].res_kv) owner[r.block] = {d, r.slot};
+  }
+  for (int d = 0; d < R_; ++d) {
+    const PlanCopy& P = plans_[d];
+    DevState& D = dev_[d];
+    const int64_t SR = D.slot_rows;
+    // 1. backward fetch payloads: Q + dO + LSE + Delta for Q blocks, K + V for KV blocks
+    for (size_t i = 0; i < P.ins.size(); ++i) {
+      Op& op = D.prog[i];
+      if (op.kind != OpKind::kCommWait || P.ins[i].division >= T) continue;
+      int recv_i = -1;
+      for (size_t k = 0; k < P.ins.size(); ++k)
+        if (P.ins[k].op == DCPX_OP_COMM_LAUNCH && !P.ins[k].send && P.ins[k].tag == op.tag) recv_i = static_cast<int>(k);
+      const Instr& RI = P.ins[recv_i];
+      const int src_dev = RI.peer;
+      const PlanCopy& S = plans_[src_dev];
+      int send_i = -1;
+      for (size_t k = 0; k < S.ins.size(); ++k)
+        if (S.ins[k].op == DCPX_OP_COMM_LAUNCH && S.ins[k].send && S.ins[k].tag == op.tag) send_i = static_cast<int>(k);
+      const Instr& SI = S.ins[send_i];
+      const DevState& A = dev_[src_dev];
+      std::vector<RowCopyJob> jobs;
+      for (int b = 0; b < RI.count; ++b) {
+        const auto rb = P.blocks[RI.offset + b];
+        const auto sb = S.blocks[SI.offset + b];
+        const auto& db = g_.data_blocks[rb.block];
+        const int rows = static_cast<int>(db.tok_end - db.tok_begin);
+        if (db.kind == DCPX_KIND_Q) {
+          jobs.push_back({reinterpret_cast<const char*>(A.q + sb.slot * SR * 128), reinterpret_cast<char*>(D.q + rb.slot * SR * 128), 256, 256, rows, 256});
+          jobs.push_back({reinterpret_cast<const char*>(A.d_o + sb.slot * SR * 128), reinterpret_cast<char*>(D.d_o + rb.slot * SR * 128), 256, 256, rows, 256});
+          jobs.push_back({reinterpret_cast<const char*>(A.lse2 + sb.slot * SR), reinterpret_cast<char*>(D.lse2 + rb.slot * SR), 4 * rows, 4 * rows, 1, 4 * rows});
+          jobs.push_back({reinterpret_cast<const char*>(A.delta + sb.slot * SR), reinterpret_cast<char*>(D.delta + rb.slot * SR), 4 * rows, 4 * rows, 1, 4 * rows});
+          bwd_send_[src_dev] += 2 * db.size_bytes; bwd_recv_[d] += 2 * db.size_bytes;  // Q + dO out
+          bwd_send_[d] += db.size_bytes; bwd_recv_[src_dev] += db.size_bytes;          // dQ back
+        } else if (db.kind == DCPX_KIND_KV) {
+          for (int h = 0; h < 2; ++h)
+            jobs.push_back({reinterpret_cast<const char*>(A.kv + (2 * sb.slot + h) * SR * 128),
+                            reinterpret_cast<char*>(D.kv + (2 * rb.slot + h) * SR * 128), 256, 256, rows, 256});
+          bwd_send_[src_dev] += db.size_bytes; bwd_recv_[d] += db.size_bytes;  // K, V out
+          bwd_send_[d] += db.size_bytes; bwd_recv_[src_dev] += db.size_bytes;  // dK, dV back
+        }
+      }
+      op.bjobs = make_jobs(d, jobs);
+    }
+    // 2. gradient returns of fetched blocks, right after the attention of their last use
+    std::map<int, int> cur_q, cur_kv;                    // slot -> fetched block
+    std::map<int, std::pair<size_t, int>> last_q, last_kv;  // block -> (attention instr, slot)
+    for (size_t i = 0; i < P.ins.size(); ++i) {
+      const Instr& I = P.ins[i];
+      if (I.op == DCPX_OP_COMM_LAUNCH && !I.send && I.division < T) {
+        for (int b = 0; b < I.count; ++b) {
+          const auto tb = P.blocks[I.offset + b];
+          const int k = g_.data_blocks[tb.block].kind;
+          if (k == DCPX_KIND_Q) cur_q[tb.slot] = tb.block;
+          else if (k == DCPX_KIND_KV) cur_kv[tb.slot] = tb.block;
+        }
+      } else if (I.op == DCPX_OP_ATTENTION) {
+        for (int k = 0; k < I.count; ++k) {
+          const auto& it = P.items[I.offset + k];
+          auto q = cur_q.find(it.q_slot);
+          if (q != cur_q.end()) last_q[q->second] = {i, it.q_slot};
+          auto kv = cur_kv.find(it.kv_slot);
+          if (kv != cur_kv.end()) last_kv[kv->second] = {i, it.kv_slot};
+        }
+      }
+    }
+    std::map<size_t, std::vector<RowCopyJob>> ret;
+    for (const auto& [block, use] : last_q) {
+      const auto [o, so] = owner.at(block);
+      const auto& db = g_.data_blocks[block];
+      ret[use.first].push_back({reinterpret_cast<const char*>(D.dq_acc + use.second * SR * 128),
+                                reinterpret_cast<char*>(dev_[o].dq_acc + so * SR * 128), 512, 512,
+                                static_cast<int32_t>(db.tok_end - db.tok_begin), 512});
+    }
+    for (const auto& [block, use] : last_kv) {
+      const auto [o, so] = owner.at(block);
+      const auto& db = g_.data_blocks[block];
+      for (int h = 0; h < 2; ++h)
+        ret[use.first].push_back({reinterpret_cast<const char*>(D.dkv_acc + (2 * use.second + h) * SR * 128),
+                                  reinterpret_cast<char*>(dev_[o].dkv_acc + (2 * so + h) * SR * 128), 512, 512,
+                                  static_cast<int32_t>(db.tok_end - db.tok_begin), 512});
+    }
+    for (auto& [i, jobs] : ret) D.prog[i].ret = make_jobs(d, jobs);
+    // 3. io: dO scatter to the resident Q slots, Delta/LSE preprocess, gradient gathers
+    std::map<std::tuple<int, int, int>, int> qslot_of;  // (seq, head, tile) -> resident Q slot
+    for (const auto& r : P.res_q) {
+      const auto& db = g_.data_blocks[r.block];
+      qslot_of[{db.seq, db.head, db.tile}] = r.slot;
+    }
+    std::vector<RowCopyJob> sdo;
+    std::vector<RowJob> prep, gq, gk, gv;
+    std::vector<int> prep_rows, gq_rows, gk_rows;
+    for (size_t k = 0; k < P.res_o.size(); ++k) {
+      const auto& db = g_.data_blocks[P.res_o[k].block];
+      auto it = qslot_of.find({db.seq, db.head, db.tile});
+      if (it == qslot_of.end()) throw Failure(DCPX_ERROR, "output block without a co-located Q block (blocks.hpp:42-51)");
+      const int64_t tok = g_.seq_offsets[db.seq] + db.tok_begin;
+      const int rows = static_cast<int>(db.tok_end - db.tok_begin);
+      sdo.push_back({reinterpret_cast<const char*>((tok * H + db.head) * 256), reinterpret_cast<char*>(D.d_o + it->second * SR * 128),
+                     H * 256, 256, rows, 256});
+      prep.push_back({D.final_o_slot[k] * SR, it->second * SR, 0, rows, 0});
+      prep_rows.push_back(rows);
+    }
+    for (const auto& r : P.res_q) {
+      const auto& db = g_.data_blocks[r.block];
+      const int64_t tok = g_.seq_offsets[db.seq] + db.tok_begin;
+      const int rows = static_cast<int>(db.tok_end - db.tok_begin);
+      gq.push_back({r.slot * SR, (tok * H + db.head) * 128, H * 128, rows, 0});
+      gq_rows.push_back(rows);
+    }
+    for (const auto& r : P.res_kv) {
+      const auto& db = g_.data_blocks[r.block];
+      const int64_t tok = g_.seq_offsets[db.seq] + db.tok_begin;
+      const int rows = static_cast<int>(db.tok_end - db.tok_begin);
+      gk.push_back({2 * r.slot * SR, (tok * G + db.head) * 128, G * 128, rows, 0});
+      gv.push_back({(2 * r.slot + 1) * SR, (tok * G + db.head) * 128, G * 128, rows, 0});
+      gk_rows.push_back(rows);
+    }
+    D.scatter_do = make_jobs(d, sdo);
+    D.prep = make_row_jobs(d, prep, prep_rows, 16);
+    D.gather_dq = make_row_jobs(d, gq, gq_rows, 16);
+    D.gather_dk = make_row_jobs(d, gk, gk_rows, 16);
+    D.gather_dv = make_row_jobs(d, gv, gk_rows, 16);
+  }
+  (void)TT;
 }
 
 // ------------------------------------------------------------------------ execution
@@ -1015,45 +1217,207 @@ void Executor::forward(void* o_out, float* lse_out, dcpx_report* rep, bool host)
     if (lse_out) CUDA_OK(cudaMemcpyAsync(lse_out, l_dev, TT * g_.H * 4, cudaMemcpyDeviceToHost, D0.cs));
     CUDA_OK(cudaStreamSynchronize(D0.cs));
   }
-  if (rep) {
-    std::memset(rep, 0, sizeof(*rep));
-    rep->devices = R_;
-    rep->stages = static_cast<int32_t>(comm_bytes_.size());
-    std::vector<double> comp_t(comm_bytes_.size(), 0), comm_t(comm_bytes_.size(), 0);
-    for (size_t t = 0; t < comm_bytes_.size(); ++t) {
-      for (const auto& [link, bytes] : comm_bytes_[t]) {
+  fill_report(rep, false);
+  fwd_done_ = true;
+}
+
+void Executor::fill_report(dcpx_report* rep, bool bwd) {
+  if (!rep) return;
+  std::memset(rep, 0, sizeof(*rep));
+  rep->devices = R_;
+  rep->stages = static_cast<int32_t>(comm_bytes_.size());
+  std::vector<double> comp_t(comm_bytes_.size(), 0), comm_t(comm_bytes_.size(), 0);
+  for (size_t t = 0; t < comm_bytes_.size(); ++t) {
+    for (const auto& [link, bytes] : comm_bytes_[t]) {
+      if (!bwd) {
         rep->total_bytes += bytes;
         rep->per_device_send[link.first] += bytes;
         rep->per_device_recv[link.second] += bytes;
-        comm_t[t] = std::max(comm_t[t], bytes ? 5e-6 + static_cast<double>(bytes) / 600e9 : 0.0);  // link_time, schedule.hpp:209-215
       }
-      for (int d = 0; d < R_; ++d) {
-        rep->total_flops += comp_flops_[t][d];
-        comp_t[t] = std::max(comp_t[t], static_cast<double>(comp_flops_[t][d]) / 312e12);  // CostParams, schedule.hpp:173-175
-      }
+      comm_t[t] = std::max(comm_t[t], bytes ? 5e-6 + static_cast<double>(bytes) / 600e9 : 0.0);  // link_time, schedule.hpp:209-215
     }
-    // pipeline_makespan (schedule.hpp:192-207)
-    double start_prev = 0, finish = 0;
-    for (size_t t = 0; t < comm_t.size(); ++t) {
-      const double start = t == 0 ? 0 : std::max(finish, start_prev + comm_t[t]);
-      start_prev = start;
-      finish = start + comp_t[t];
-    }
-    rep->makespan = finish;
-    rep->wire_bytes = rep->total_bytes;
-    for (int d = 0; d < R_; ++d) rep->kernel_launches += dev_[d].launches;
-    if (opt.timing) {
-      double mx = 0;
-      for (auto& D : dev_) {
-        DeviceGuard gd(D.ordinal);
-        CUDA_OK(cudaEventSynchronize(D.t1));
-        float ms = 0;
-        CUDA_OK(cudaEventElapsedTime(&ms, D.t0, D.t1));
-        mx = std::max<double>(mx, ms);
-      }
-      rep->device_ms = mx;
+    for (int d = 0; d < R_; ++d) {
+      rep->total_flops += comp_flops_[t][d];
+      comp_t[t] = std::max(comp_t[t], static_cast<double>(comp_flops_[t][d]) / 312e12);  // CostParams, schedule.hpp:173-175
     }
   }
+  // pipeline_makespan (schedule.hpp:192-207)
+  double start_prev = 0, finish = 0;
+  for (size_t t = 0; t < comm_t.size(); ++t) {
+    const double start = t == 0 ? 0 : std::max(finish, start_prev + comm_t[t]);
+    start_prev = start;
+    finish = start + comp_t[t];
+  }
+  rep->makespan = finish;
+  if (bwd) {
+    // backward: 5 GEMMs per attended pair vs 2 forward -> 2.5x FLOPs; planned bytes =
+    // (Q + dO out, dQ back) per Q fetch and (KV out, dK/dV back) per KV fetch
+    rep->total_flops = rep->total_flops / 2 * 5;
+    rep->makespan = 0;
+    for (int d = 0; d < R_; ++d) {
+      rep->per_device_send[d] = bwd_send_[d];
+      rep->per_device_recv[d] = bwd_recv_[d];
+      rep->total_bytes += bwd_send_[d];
+    }
+  }
+  rep->wire_bytes = rep->total_bytes;
+  for (int d = 0; d < R_; ++d) rep->kernel_launches += dev_[d].launches;
+  if (opt.timing) {
+    double mx = 0;
+    for (auto& D : dev_) {
+      DeviceGuard gd(D.ordinal);
+      CUDA_OK(cudaEventSynchronize(D.t1));
+      float ms = 0;
+      CUDA_OK(cudaEventElapsedTime(&ms, D.t0, D.t1));
+      mx = std::max<double>(mx, ms);
+    }
+    rep->device_ms = mx;
+  }
+}
+
+void Executor::backward(const void* d_o, void* dq, void* dk, void* dv, dcpx_report* rep, bool host) {
+  if (!prepared_) throw Failure(DCPX_ERROR, "dcpx_backward before dcpx_prepare");
+  if (!fwd_done_) throw Failure(DCPX_ERROR, "dcpx_backward needs a preceding dcpx_forward");
+  const int64_t TT = g_.total_tokens(), H = g_.H, G = g_.G;
+  const int T = R_ ? plans_[0].divisions : 0;
+  const char* ddo = static_cast<const char*>(d_o);
+  char *ddq = static_cast<char*>(dq), *ddk = static_cast<char*>(dk), *ddv = static_cast<char*>(dv);
+  const size_t bq = TT * H * 256, bk = TT * G * 256;
+  for (auto& D : dev_) {
+    D.next_event = 0;
+    D.launches = 0;
+    DeviceGuard gd(D.ordinal);
+    if (opt.timing) CUDA_OK(cudaEventRecord(D.t0, D.cs));
+  }
+  if (host) {
+    DevState& D0 = dev_[0];
+    DeviceGuard gd(D0.ordinal);
+    if (!bwd_stage_) bwd_stage_ = static_cast<char*>(alloc(0, 2 * bq + 2 * bk));
+    CUDA_OK(cudaMemcpyAsync(bwd_stage_, d_o, bq, cudaMemcpyHostToDevice, D0.cs));
+    cudaEvent_t e = event(0);
+    CUDA_OK(cudaEventRecord(e, D0.cs));
+    for (int d = 1; d < R_; ++d) {
+      DeviceGuard g2(dev_[d].ordinal);
+      CUDA_OK(cudaStreamWaitEvent(dev_[d].cs, e, 0));
+    }
+    ddo = bwd_stage_;
+    ddq = bwd_stage_ + bq;
+    ddk = bwd_stage_ + 2 * bq;
+    ddv = bwd_stage_ + 2 * bq + bk;
+  }
+  const float scale = static_cast<float>(1.0 / std::sqrt(static_cast<double>(g_.D)));
+  for (int d = 0; d < R_; ++d) {
+    DevState& D = dev_[d];
+    DeviceGuard gd(D.ordinal);
+    const int64_t SR = D.slot_rows;
+    CUDA_OK(cudaMemsetAsync(D.dq_acc, 0, std::max<int64_t>(1, D.cap_q) * SR * 512, D.cs));
+    CUDA_OK(cudaMemsetAsync(D.dkv_acc, 0, std::max<int64_t>(1, D.cap_kv) * 2 * SR * 512, D.cs));
+    launch_row_copy(D.scatter_do.dj, D.cs, reinterpret_cast<int64_t>(ddo), 0);
+    launch_delta(D.prep.dj, D.o, D.lse, D.d_o, D.delta, D.lse2, D.cs);
+    D.launches += 2;
+  }
+  // every device's accumulators are zeroed before any peer returns into them
+  {
+    std::vector<cudaEvent_t> ev(static_cast<size_t>(R_));
+    for (int d = 0; d < R_; ++d) {
+      DeviceGuard gd(dev_[d].ordinal);
+      ev[d] = event(d);
+      CUDA_OK(cudaEventRecord(ev[d], dev_[d].cs));
+    }
+    for (int d = 0; d < R_; ++d)
+      for (int e = 0; e < R_; ++e)
+        if (e != d) {
+          DeviceGuard gd(dev_[d].ordinal);
+          CUDA_OK(cudaStreamWaitEvent(dev_[d].cs, ev[e], 0));
+        }
+  }
+  std::map<std::string, cudaEvent_t> send_ev, recv_ev;
+  for (const auto& [d, i] : order_) {
+    DevState& D = dev_[d];
+    Op& op = D.prog[i];
+    if (plans_[d].ins[i].division >= T) continue;  // output stage has no backward counterpart
+    DeviceGuard gd(D.ordinal);
+    switch (op.kind) {
+      case OpKind::kFwdAttn: {
+        if (op.bnum_units) {
+          BwdParams p{};
+          p.units = op.bunits; p.steps = op.bsteps; p.items = op.bitems; p.ranges = D.ranges;
+          p.lse2 = D.lse2; p.delta = D.delta; p.dq_acc = D.dq_acc; p.dkv_acc = D.dkv_acc;
+          p.num_units = op.bnum_units;
+          p.slot_rows = static_cast<int32_t>(D.slot_rows);
+          p.scale_log2 = static_cast<float>(1.4426950408889634) * scale;
+          p.scale = scale;
+          launch_attn_bwd(D.tm_q, D.tm_do, D.tm_kv, p, op.bgrid, D.cs);
+          ++D.launches;
+        }
+        if (op.ret.dj.n_blocks) {
+          launch_return_accum(op.ret.dj, D.cs);
+          ++D.launches;
+        }
+        break;
+      }
+      case OpKind::kCommLaunch: {
+        cudaEvent_t e = event(d);
+        CUDA_OK(cudaEventRecord(e, D.cs));
+        (op.send ? send_ev : recv_ev)[op.tag] = e;
+        break;
+      }
+      case OpKind::kCommWait: {
+        CUDA_OK(cudaStreamWaitEvent(D.ms, send_ev.at(op.tag), 0));
+        CUDA_OK(cudaStreamWaitEvent(D.ms, recv_ev.at(op.tag), 0));
+        launch_row_copy(op.bjobs.dj, D.ms);
+        ++D.launches;
+        cudaEvent_t e = event(d);
+        CUDA_OK(cudaEventRecord(e, D.ms));
+        CUDA_OK(cudaStreamWaitEvent(D.cs, e, 0));
+        break;
+      }
+      default:
+        break;
+    }
+  }
+  // all gradient returns land before the owners convert their accumulators
+  {
+    std::vector<cudaEvent_t> ev(static_cast<size_t>(R_));
+    for (int d = 0; d < R_; ++d) {
+      DeviceGuard gd(dev_[d].ordinal);
+      ev[d] = event(d);
+      CUDA_OK(cudaEventRecord(ev[d], dev_[d].cs));
+    }
+    for (int d = 0; d < R_; ++d)
+      for (int e = 0; e < R_; ++e)
+        if (e != d) {
+          DeviceGuard gd(dev_[d].ordinal);
+          CUDA_OK(cudaStreamWaitEvent(dev_[d].cs, ev[e], 0));
+        }
+  }
+  for (int d = 0; d < R_; ++d) {
+    DevState& D = dev_[d];
+    DeviceGuard gd(D.ordinal);
+    if (ddq) { launch_to_bf16(D.gather_dq.dj, D.dq_acc, reinterpret_cast<__nv_bfloat16*>(ddq), D.cs); ++D.launches; }
+    if (ddk) { launch_to_bf16(D.gather_dk.dj, D.dkv_acc, reinterpret_cast<__nv_bfloat16*>(ddk), D.cs); ++D.launches; }
+    if (ddv) { launch_to_bf16(D.gather_dv.dj, D.dkv_acc, reinterpret_cast<__nv_bfloat16*>(ddv), D.cs); ++D.launches; }
+    if (opt.timing) CUDA_OK(cudaEventRecord(D.t1, D.cs));
+    CUDA_OK(cudaGetLastError());
+  }
+  if (host) {
+    DevState& D0 = dev_[0];
+    for (int d = 1; d < R_; ++d) {
+      cudaEvent_t e = event(d);
+      {
+        DeviceGuard g2(dev_[d].ordinal);
+        CUDA_OK(cudaEventRecord(e, dev_[d].cs));
+      }
+      DeviceGuard g3(D0.ordinal);
+      CUDA_OK(cudaStreamWaitEvent(D0.cs, e, 0));
+    }
+    DeviceGuard gd(D0.ordinal);
+    if (dq) CUDA_OK(cudaMemcpyAsync(dq, ddq, bq, cudaMemcpyDeviceToHost, D0.cs));
+    if (dk) CUDA_OK(cudaMemcpyAsync(dk, ddk, bk, cudaMemcpyDeviceToHost, D0.cs));
+    if (dv) CUDA_OK(cudaMemcpyAsync(dv, ddv, bk, cudaMemcpyDeviceToHost, D0.cs));
+    CUDA_OK(cudaStreamSynchronize(D0.cs));
+  }
+  fill_report(rep, true);
 }
 
 void Executor::synchronize() {

@@ -70,6 +70,13 @@ struct Op {
   // kMerge / kCopy
   JobList jobs;
   int32_t* src_rows = nullptr;
+  // backward of an attention instruction (K1b) + gradient returns that follow it
+  BwdUnit* bunits = nullptr;
+  BwdStep* bsteps = nullptr;
+  ItemMask* bitems = nullptr;
+  int bnum_units = 0, bgrid = 0;
+  JobList ret;   // LOCAL: dQ / dK,dV partials of fetched blocks whose last use is here
+  JobList bjobs; // kCommWait: backward payload transfer (Q + dO + LSE + Delta, or K + V)
   // comm
   int send = 0, peer = 0;
   std::string tag;
@@ -89,6 +96,11 @@ struct DevState {
   CUtensorMap tm_q{}, tm_kv{};
   std::vector<Op> prog;
   JobList scatter_q, scatter_k, scatter_v, gather_o, gather_lse;
+  // backward arenas (parallel to Q / KV arenas) and their io jobs
+  __nv_bfloat16* d_o = nullptr;
+  float *lse2 = nullptr, *delta = nullptr, *dq_acc = nullptr, *dkv_acc = nullptr;
+  CUtensorMap tm_do{};
+  JobList scatter_do, prep, gather_dq, gather_dk, gather_dv;
   std::vector<int32_t> final_o_slot;  // per resident_o entry: physical slot holding the result
   std::vector<cudaEvent_t> events;
   size_t next_event = 0;
@@ -111,6 +123,7 @@ class Executor {
                const dcpx_mask_view* m);
   void load_inputs(const void* q, const void* k, const void* v, bool host);
   void forward(void* o_out, float* lse_out, dcpx_report* rep, bool host);
+  void backward(const void* d_o, void* dq, void* dk, void* dv, dcpx_report* rep, bool host);
   void synchronize();
   void debug_arena(int dev, int kind, void** ptr, int64_t* rows);
   Options opt;
@@ -120,6 +133,8 @@ class Executor {
   void compile_device(int d);
   void compile_attention(int d, int ins_index, std::vector<bool>& fused_red);
   void build_io_jobs(int d);
+  void build_bwd_jobs();
+  void fill_report(dcpx_report* rep, bool bwd);
   void simulate_order();
   cudaEvent_t event(int d);
   void free_all();
@@ -135,6 +150,9 @@ class Executor {
   std::vector<int> alloc_dev_;
   char* in_stage_ = nullptr;   // host-input staging on device 0 (load_inputs_host)
   char* out_stage_ = nullptr;  // host-output staging on device 0 (forward_host)
+  char* bwd_stage_ = nullptr;  // host staging for backward (dO in, dQ/dK/dV out)
+  bool fwd_done_ = false;
+  std::vector<uint64_t> bwd_send_, bwd_recv_;  // planned backward bytes per device
   bool prepared_ = false;
   // report
   std::vector<std::map<std::pair<int, int>, uint64_t>> comm_bytes_;

@@ -93,10 +93,12 @@ __global__ void merge_kernel(const MergeJob* __restrict__ jobs, const int32_t* _
   if (sub == 0) lse_arena[(int64_t)J.dst_row0 + row_in_job] = lse_out;
 }
 
-// Delta[row] = sum_d dO[row][d] * O[row][d] (fp32), one 16-lane group per row.
+// Backward preprocess for one resident output block: Delta[row] = sum_d dO[row][d] * O[row][d]
+// and LSE in log2 units, written at the block's Q-arena rows. One 16-lane group per row.
 __global__ void delta_kernel(const RowJob* __restrict__ jobs, const int32_t* __restrict__ job_of_block,
                              const int32_t* __restrict__ first_chunk, const __nv_bfloat16* o_arena,
-                             const __nv_bfloat16* do_arena, float* delta) {
+                             const float* lse_arena, const __nv_bfloat16* do_arena, float* delta,
+                             float* lse2) {
   const int b = blockIdx.x;
   const int j = job_of_block[b];
   const RowJob J = jobs[j];
@@ -116,7 +118,31 @@ __global__ void delta_kernel(const RowJob* __restrict__ jobs, const int32_t* __r
   }
 #pragma unroll
   for (int o = 8; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-  if (r < J.rows && sub == 0) delta[(int64_t)J.b_row0 + r] = s;
+  if (r < J.rows && sub == 0) {
+    delta[(int64_t)J.b_row0 + r] = s;
+    lse2[(int64_t)J.b_row0 + r] = lse_arena[(int64_t)J.a_row0 + r] * 1.4426950408889634f;
+  }
+}
+
+// Gradient return (LOCAL transport): dst[i] += src[i] atomically (dst may be a peer
+// device's accumulator over NVLink), then src[i] = 0 so the slot can be reused.
+__global__ void return_accum_kernel(const RowCopyJob* __restrict__ jobs, const int32_t* __restrict__ job_of_block,
+                                    const int32_t* __restrict__ first_chunk) {
+  const int b = blockIdx.x;
+  const int j = job_of_block[b];
+  const RowCopyJob J = jobs[j];
+  const int r0 = (b - first_chunk[j]) * kRowsPerChunk;
+  const int r1 = min(J.rows, r0 + kRowsPerChunk);
+  float* src = reinterpret_cast<float*>(const_cast<char*>(J.src));
+  float* dst = reinterpret_cast<float*>(J.dst);
+  for (int i = r0 * 32 + threadIdx.x; i < r1 * 32; i += blockDim.x) {  // rows of 128 floats, float4 each
+    float4* s4 = reinterpret_cast<float4*>(src) + i;
+    const float4 v = *s4;
+    asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(reinterpret_cast<float4*>(dst) + i),
+                 "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
+                 : "memory");
+    *s4 = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
 }
 
 // dst_f32[row][c] += bf16 src[row][c] (returned partial gradients), rows of 128.
@@ -172,8 +198,16 @@ void launch_row_copy(const DevJobs& j, cudaStream_t s, int64_t src_adjust, int64
 void launch_merge(const DevJobs& j, const int32_t* src_rows, __nv_bfloat16* o, float* lse, cudaStream_t s) {
   if (j.n_blocks) merge_kernel<<<j.n_blocks, 256, 0, s>>>(static_cast<const MergeJob*>(j.jobs), src_rows, j.job_of_block, j.first_chunk, o, lse);
 }
-void launch_delta(const DevJobs& j, const __nv_bfloat16* o, const __nv_bfloat16* d_o, float* delta, cudaStream_t s) {
-  if (j.n_blocks) delta_kernel<<<j.n_blocks, 256, 0, s>>>(static_cast<const RowJob*>(j.jobs), j.job_of_block, j.first_chunk, o, d_o, delta);
+void launch_delta(const DevJobs& j, const __nv_bfloat16* o, const float* lse, const __nv_bfloat16* d_o,
+                  float* delta, float* lse2, cudaStream_t s) {
+  if (j.n_blocks)
+    delta_kernel<<<j.n_blocks, 256, 0, s>>>(static_cast<const RowJob*>(j.jobs), j.job_of_block, j.first_chunk, o,
+                                            lse, d_o, delta, lse2);
+}
+void launch_return_accum(const DevJobs& j, cudaStream_t s) {
+  if (j.n_blocks)
+    return_accum_kernel<<<j.n_blocks, 256, 0, s>>>(static_cast<const RowCopyJob*>(j.jobs), j.job_of_block,
+                                                   j.first_chunk);
 }
 void launch_accum(const DevJobs& j, const __nv_bfloat16* src, float* dst, cudaStream_t s) {
   if (j.n_blocks) accum_bf16_kernel<<<j.n_blocks, 256, 0, s>>>(static_cast<const RowJob*>(j.jobs), j.job_of_block, j.first_chunk, src, dst);

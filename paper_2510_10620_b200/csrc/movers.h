@@ -40,10 +40,15 @@ struct DevJobs {
 
 void launch_row_copy(const DevJobs& j, cudaStream_t s, int64_t src_adjust = 0, int64_t dst_adjust = 0);
 void launch_merge(const DevJobs& j, const int32_t* src_rows, __nv_bfloat16* o, float* lse, cudaStream_t s);
-void launch_delta(const DevJobs& j, const __nv_bfloat16* o, const __nv_bfloat16* d_o, float* delta, cudaStream_t s);
+void launch_delta(const DevJobs& j, const __nv_bfloat16* o, const float* lse, const __nv_bfloat16* d_o,
+                  float* delta, float* lse2, cudaStream_t s);
+// jobs: RowCopyJob with src/dst = fp32 accumulators, rows of 128 floats (row_bytes ignored)
+void launch_return_accum(const DevJobs& j, cudaStream_t s);
 void launch_accum(const DevJobs& j, const __nv_bfloat16* src, float* dst, cudaStream_t s);
 void launch_to_bf16(const DevJobs& j, const float* src, __nv_bfloat16* dst, cudaStream_t s);
 
+void launch_attn_bwd(const CUtensorMap& tm_q, const CUtensorMap& tm_do, const CUtensorMap& tm_kv,
+                     const BwdParams& p, int grid, cudaStream_t stream);
 void launch_attn_fwd(const CUtensorMap& tm_q, const CUtensorMap& tm_kv, const FwdParams& p, int grid,
                      cudaStream_t stream);
 

@@ -65,6 +65,39 @@ struct CopySeg {
   int64_t bytes;  // multiple of 16
 };
 
+// One backward work unit: a 128-row kv sub-tile of one KV slot, streaming all q tiles
+// of all items of the division that read it.
+struct BwdUnit {
+  int32_t kv_row0;  // KV arena row of the K sub-tile (V and the dV accumulator at + slot_rows)
+  int32_t n_kv;     // valid kv rows (1..128)
+  int32_t step_begin;
+  int32_t step_count;
+};
+
+struct BwdStep {
+  int32_t q_row0;    // Q / dO / LSE / Delta / dQ-accumulator row of this 128-row q tile
+  int32_t n_q;       // valid q rows (1..128)
+  int32_t item;      // ItemMask index
+  int32_t q_local0;  // q row index within the item of tile row 0
+  int32_t col0;      // kv-tile-relative index of the unit's kv row 0
+  uint32_t cls;      // kTileEmpty / kTilePartial / kTileFull
+};
+
+struct BwdParams {
+  const BwdUnit* units;
+  const BwdStep* steps;
+  const ItemMask* items;
+  const int32_t* ranges;
+  const float* lse2;   // LSE * log2(e) per Q-arena row
+  const float* delta;  // rowsum(dO o O) per Q-arena row
+  float* dq_acc;       // [Q-arena rows][128] fp32
+  float* dkv_acc;      // [KV-arena rows][128] fp32
+  int32_t num_units;
+  int32_t slot_rows;
+  float scale_log2;
+  float scale;
+};
+
 struct FwdParams {
   const FwdUnit* units;
   const FwdStep* steps;

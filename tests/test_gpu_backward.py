@@ -1,0 +1,86 @@
+"""GPU parity of the backward executor (K1b + fetch/return exchange) against the dense
+FP64 backward restatement (oracle/dcp_oracle.c:orc_dense_backward) on the same bf16
+inputs. Tolerance (north_star): max relative error <= 2e-2 on dQ, dK, dV."""
+import numpy as np
+import pytest
+
+import oracle as O
+from paper_2510_10620_b200 import planner as PL
+from paper_2510_10620_b200.executor import DCPExecutor
+
+from common import MIXED_SPECS, O_TOL, bundle_for, inputs, rel_err
+
+pytestmark = pytest.mark.gpu
+
+
+def _fwd_bwd(bundle, q, k, v, d_o):
+    import torch
+    ex = DCPExecutor([0] * bundle.R)
+    ex.prepare(bundle)
+    T, H, G = bundle.total_tokens, bundle.H, bundle.G
+    o = torch.zeros((T, H, 128), dtype=torch.bfloat16, device="cuda")
+    lse = torch.zeros((H, T), device="cuda")
+    dq = torch.zeros((T, H, 128), dtype=torch.bfloat16, device="cuda")
+    dk = torch.zeros((T, G, 128), dtype=torch.bfloat16, device="cuda")
+    dv = torch.zeros((T, G, 128), dtype=torch.bfloat16, device="cuda")
+    ex.load_inputs(q.cuda(), k.cuda(), v.cuda())
+    ex.forward(o, lse)
+    rep = ex.backward(d_o.cuda(), dq, dk, dv)
+    ex.synchronize()
+    ex.close()
+    return [t.float().cpu().numpy() for t in (o, dq, dk, dv)], rep
+
+
+def _d_o(bundle, seed):
+    import torch
+    g = torch.Generator().manual_seed(1000 + seed)
+    return torch.randn((bundle.total_tokens, bundle.H, 128), generator=g).to(torch.bfloat16)
+
+
+@pytest.mark.parametrize("R", [1, 2, 4])
+def test_backward_mixed_masks_vs_dense(R):
+    bundle = bundle_for(MIXED_SPECS, H=4, G=2, block=256, R=R)
+    (q, k, v), (q64, k64, v64) = inputs(bundle, seed=R)
+    d_o = _d_o(bundle, R)
+    (o, dq, dk, dv), rep = _fwd_bwd(bundle, q, k, v, d_o)
+    rq, rk, rv = O.dense_backward(bundle, q64, k64, v64, d_o.double().numpy())
+    assert rel_err(dq, rq) <= O_TOL
+    assert rel_err(dk, rk) <= O_TOL
+    assert rel_err(dv, rv) <= O_TOL
+    assert rep["total_flops"] == bundle.total_flops // 2 * 5
+    send, recv = bundle.bwd_bytes()
+    assert rep["per_device_send"] == [int(x) for x in send]
+    assert rep["per_device_recv"] == [int(x) for x in recv]
+
+
+@pytest.mark.parametrize("block", [128, 512])
+def test_backward_ragged_and_gqa(block):
+    specs = [PL.SeqSpec(1000), PL.SeqSpec(77, "lambda", sink=5, window=20), PL.SeqSpec(1),
+             PL.SeqSpec(513, "shared_question", question_len=100, answer_lens=[200, 213])]
+    bundle = bundle_for(specs, H=4, G=1, block=block, R=2)
+    (q, k, v), (q64, k64, v64) = inputs(bundle, seed=block)
+    d_o = _d_o(bundle, block)
+    (o, dq, dk, dv), _ = _fwd_bwd(bundle, q, k, v, d_o)
+    rq, rk, rv = O.dense_backward(bundle, q64, k64, v64, d_o.double().numpy())
+    assert rel_err(dq, rq) <= O_TOL
+    assert rel_err(dk, rk) <= O_TOL
+    assert rel_err(dv, rv) <= O_TOL
+
+
+def test_backward_fuzz_random_batches():
+    for seed in range(5):
+        b = PL.Batch.random(100 + seed, max_seq_len=600, max_seqs=3, max_heads=2, head_dim=128)
+        R = 1 + seed % 3
+        try:
+            bundle = PL.plan(b, R, 128, eps_intra=0.5, eps_data=0.6, eps_inter=0.5, seed=seed)
+        except PL.PlannerError as e:
+            if e.kind == "InfeasibleError":
+                continue
+            raise
+        (q, k, v), (q64, k64, v64) = inputs(bundle, seed=seed)
+        d_o = _d_o(bundle, seed)
+        (o, dq, dk, dv), _ = _fwd_bwd(bundle, q, k, v, d_o)
+        rq, rk, rv = O.dense_backward(bundle, q64, k64, v64, d_o.double().numpy())
+        assert rel_err(dq, rq) <= O_TOL, seed
+        assert rel_err(dk, rk) <= O_TOL, seed
+        assert rel_err(dv, rv) <= O_TOL, seed

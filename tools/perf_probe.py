@@ -1,0 +1,42 @@
+"""Quick device-time probe of the executor on a cached plan (not the bench contract).
+    python tools/perf_probe.py cfg2_R1 [iters]"""
+import os
+import sys
+
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, REPO)
+sys.path.insert(0, os.path.join(REPO, "tools"))
+
+import torch  # noqa: E402
+
+from make_plans import load  # noqa: E402
+from paper_2510_10620_b200.executor import DCPExecutor  # noqa: E402
+
+
+def main():
+    name = sys.argv[1] if len(sys.argv) > 1 else "cfg2_R1"
+    iters = int(sys.argv[2]) if len(sys.argv) > 2 else 10
+    b = load(name)
+    T, H, G = b.total_tokens, b.H, b.G
+    g = torch.Generator(device="cuda").manual_seed(0)
+    q = torch.randn((T, H, 128), device="cuda", generator=g).to(torch.bfloat16)
+    k = torch.randn((T, G, 128), device="cuda", generator=g).to(torch.bfloat16)
+    v = torch.randn((T, G, 128), device="cuda", generator=g).to(torch.bfloat16)
+    ex = DCPExecutor([0] * b.R)
+    ex.prepare(b)
+    o = torch.empty((T, H, 128), dtype=torch.bfloat16, device="cuda")
+    lse = torch.empty((H, T), device="cuda")
+    ex.load_inputs(q, k, v)
+    for _ in range(3):
+        rep = ex.forward(o, lse)
+    times = []
+    for _ in range(iters):
+        rep = ex.forward(o, lse)
+        times.append(rep["device_ms"])
+    ms = min(times)
+    print(f"{name}: fwd flops {b.total_flops / 1e12:.3f} T  device {ms:.3f} ms (median {sorted(times)[len(times)//2]:.3f})"
+          f"  -> {b.total_flops / ms / 1e9:.1f} TFLOP/s  launches {rep['kernel_launches']}")
+
+
+if __name__ == "__main__":
+    main()
