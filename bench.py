@@ -1,0 +1,332 @@
+"""bench.py — DCP executor fwd+bwd throughput on B200 (BASELINE.json metric).
+
+Workload (BASELINE.json configs[1]): 8B-GPT attention layer, 32 query / 8 KV heads, d 128,
+causal mask, LongAlign-like skewed lengths, 64K-token batch (synth seed 42, make_batches
+budget 65536, batch index 2: 6 sequences, 63,855 tokens), block 1024, T = 4 divisions,
+planned by the reference planner for R = N devices (plans/cfg2_R{N}.npz; planning is never
+timed). One step = load packed bf16 Q/K/V into the slot arenas + forward + backward of the
+whole plan. FLOPs count only attended pairs: F_fwd = 4 * D * pairs (blocks.hpp:191),
+F_total = 3.5 * F_fwd.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl dcpx|reference] [--config cfg2]
+
+N > 1 (launched by torchrun): the multi-GPU plan is executed on N GPUs by rank 0's
+context, which owns all N devices (LOCAL transport: peer-to-peer copies over NVLink);
+timing is the max over the devices. Other ranks join the barriers only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+sys.path.insert(0, os.path.join(REPO, "tools"))
+
+PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
+
+
+def peaks():
+    try:
+        with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return p, "measured"
+    except Exception:  # noqa: BLE001
+        return PEAKS_FALLBACK, "fallback"
+
+
+class ClockSampler:
+    """Samples nvidia-smi SM clocks and throttle reasons during the timed region."""
+
+    def __init__(self, gpus):
+        self.gpus = gpus
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                                      "-i", ",".join(str(g) for g in self.gpus)],
+                                     capture_output=True, text=True, timeout=5).stdout
+                for line in out.strip().splitlines():
+                    f = [x.strip() for x in line.split(",")]
+                    if len(f) >= 6:
+                        self.samples.append(f)
+            except Exception:  # noqa: BLE001
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = sorted(float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit())
+        mx = max((float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()), default=None)
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[2 + i].lower() == "active"})
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx, "reasons": reasons}
+
+
+def load_bundle(name):
+    from make_plans import load
+    return load(name)
+
+
+def cpu_baseline(bundle, seconds_target=15.0):
+    """Reference exec_attention (simexec.hpp:33-76, the reference's CPU executor hot loop)
+    on a deterministic sample of this plan's AttentionItems, all host threads."""
+    import numpy as np
+
+    import oracle as O
+    if not O.ref_available():
+        return None
+    threads = os.cpu_count() or 1
+    items = []
+    for dp in bundle.devices:
+        for ins in dp.instructions():
+            if ins["op"] == 0:
+                items.extend(dp.items[ins["offset"]: ins["offset"] + ins["count"]])
+    # every k-th item, ~1.68 GFLOP/s/core for FP64 exec_attention
+    per_item = float(np.mean([(it["q_end"] - it["q_begin"]) * (it["kv_end"] - it["kv_begin"]) for it in items]))
+    budget_flops = seconds_target * threads * 1.5e9
+    n = max(threads, min(len(items), int(budget_flops / (4 * 128 * per_item * 0.6))))
+    stride = max(1, len(items) // n)
+    sample = items[::stride][:n]
+    nq, nk, offs, rows, flops = [], [], [], [], 0
+    off = 0
+    for it in sample:
+        r = O.item_rows(bundle, int(it["seq"]), int(it["q_begin"]), int(it["q_end"]),
+                        int(it["kv_begin"]), int(it["kv_end"]))
+        nq.append(len(r)); nk.append(int(it["kv_end"] - it["kv_begin"])); offs.append(off)
+        rows.append(r); off += len(r)
+        flops += 4 * 128 * int(np.maximum(r[:, 1] - r[:, 0], 0).sum() + np.maximum(r[:, 3] - r[:, 2], 0).sum())
+    sec = O.ref_time_items(nq, nk, offs, np.concatenate(rows), 128, threads)
+    return {"value": flops / sec / 1e12, "unit": "TFLOP/s", "cores": threads, "kind": "reference",
+            "sample": f"reference exec_attention (FP64, forward only: the reference has no backward) on "
+                      f"{len(sample)} of {len(items)} AttentionItems (every {stride}th), {flops / 1e9:.1f} GFLOP "
+                      f"in {sec:.2f}s on {threads} host threads",
+            "seconds": sec, "flops": flops}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="dcpx", choices=["dcpx", "reference"])
+    ap.add_argument("--config", default="cfg2")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    N = args.gpus
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("gloo", init_method="env://")
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+
+    name = f"{args.config}_R{N}"
+    metric = "masked attention fwd+bwd TFLOPS"
+    config = {"workload": f"{args.config}: 8B-GPT attention layer (32 q / 8 kv heads, d 128), causal, "
+                          "LongAlign-skewed 64K-token batch (6 seqs, 63,855 tokens), block 1024, T 4, "
+                          f"DCP plan for {N} device(s)", "global_batch_tokens": None, "heads": "32/8",
+              "block": 1024, "parallelism": f"dcp{N}", "l2": "inputs larger than L2 (q alone 523 MB)"}
+
+    if args.impl == "reference":
+        if rank != 0:
+            barrier()
+            return
+        bundle = load_bundle(name)
+        config["global_batch_tokens"] = bundle.total_tokens
+        vals = []
+        for i in range(args.warmup + args.steps):
+            cb = cpu_baseline(bundle, seconds_target=12.0 / max(1, (args.warmup + args.steps) / 4))
+            if cb is None:
+                print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libdcpref.so not built"}))
+                barrier()
+                return
+            if i >= args.warmup:
+                vals.append(cb)
+        v = sum(c["value"] for c in vals) / len(vals)
+        ms = 3.5 * bundle.total_flops / (v * 1e12) * 1e3
+        line = {"impl": "reference", "metric": metric, "value": v, "unit": "TFLOP/s", "n_gpus": N,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": config,
+                "cpu_baseline": {k: vals[-1][k] for k in ("kind", "cores", "sample")} | {"value": v, "unit": "TFLOP/s"},
+                "e2e": {"value": v, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        barrier()
+        return
+
+    import torch
+
+    if rank != 0:
+        barrier()   # bundle ready
+        barrier()   # timed region start
+        barrier()   # timed region end
+        return
+
+    from paper_2510_10620_b200.executor import DCPExecutor
+
+    bundle = load_bundle(name)
+    T, H, G = bundle.total_tokens, bundle.H, bundle.G
+    config["global_batch_tokens"] = T
+    F_fwd = bundle.total_flops
+    F_total = 3.5 * F_fwd
+    torch.cuda.set_device(0)
+    g = torch.Generator(device="cuda").manual_seed(0)
+    q = torch.randn((T, H, 128), device="cuda", generator=g).to(torch.bfloat16)
+    k = torch.randn((T, G, 128), device="cuda", generator=g).to(torch.bfloat16)
+    v = torch.randn((T, G, 128), device="cuda", generator=g).to(torch.bfloat16)
+    d_o = torch.randn((T, H, 128), device="cuda", generator=g).to(torch.bfloat16)
+    o = torch.empty_like(q)
+    lse = torch.empty((H, T), device="cuda")
+    dq, dk, dv = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
+
+    ex = DCPExecutor(list(range(N)))
+    ex.set_option("kernel_timing", 1)
+    ex.prepare(bundle)
+    barrier()
+
+    def step():
+        ex.load_inputs(q, k, v)
+        rf = ex.forward(o, lse)
+        rb = ex.backward(d_o, dq, dk, dv)
+        return rf, rb
+
+    for _ in range(args.warmup):
+        step()
+    for d in range(N):
+        torch.cuda.synchronize(d)
+    barrier()
+    fwd_ms, bwd_ms, fwd_k, bwd_k, launches = [], [], [], [], 0
+    with ClockSampler(list(range(N))) as clk:
+        starts = [torch.cuda.Event(enable_timing=True) for _ in range(N)]
+        ends = [torch.cuda.Event(enable_timing=True) for _ in range(N)]
+        for d in range(N):
+            with torch.cuda.device(d):
+                torch.cuda.synchronize(d)
+                starts[d].record()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            rf, rb = step()
+            fwd_ms.append(rf["device_ms"]); bwd_ms.append(rb["device_ms"])
+            fwd_k.append(rf["attn_ms"]); bwd_k.append(rb["attn_ms"])
+            launches += rf["kernel_launches"] + rb["kernel_launches"] + 3 * N  # + q/k/v scatters
+        for d in range(N):
+            with torch.cuda.device(d):
+                ends[d].record()
+                torch.cuda.synchronize(d)
+        wall = time.perf_counter() - t0
+    barrier()
+    # executor events bracket each call on every device (max over devices); the torch events
+    # on the default stream bracket the whole region per device
+    total_ms = max(starts[d].elapsed_time(ends[d]) for d in range(N))
+    ms_step = max(total_ms / args.steps, (sum(fwd_ms) + sum(bwd_ms)) / args.steps)
+    value = F_total / (ms_step * 1e-3) / 1e12
+
+    # roofline of the dominant kernel (backward attention, K1b) and of the forward (K1)
+    pk, src = peaks()
+    peak = pk.get("bf16_tflops_sustained", pk["bf16_tflops"])
+    bwd_kernel_ms = sum(bwd_k) / len(bwd_k)
+    fwd_kernel_ms = sum(fwd_k) / len(fwd_k)
+    bwd_flops, fwd_flops = 2.5 * F_fwd, F_fwd
+    dominant = "attn_bwd_kernel" if bwd_kernel_ms >= fwd_kernel_ms else "attn_fwd_kernel"
+    if dominant == "attn_bwd_kernel":
+        ach = bwd_flops / (bwd_kernel_ms * 1e-3) / 1e12
+    else:
+        ach = fwd_flops / (fwd_kernel_ms * 1e-3) / 1e12
+    traffic = None
+    tpath = os.path.join(REPO, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get(f"{name}:{dominant}")
+        except Exception:  # noqa: BLE001
+            traffic = None
+    roof = {"bound": "tensor", "kernel": dominant, "achieved": ach, "peak": peak, "unit": "TFLOP/s",
+            "frac": ach / peak, "traffic": traffic,
+            "peak_source": f"{src} bf16_tflops_sustained (kernel timed inside a long step)",
+            "per_kernel": {"attn_fwd_kernel": {"ms": fwd_kernel_ms, "tflops": fwd_flops / (fwd_kernel_ms * 1e-3) / 1e12},
+                           "attn_bwd_kernel": {"ms": bwd_kernel_ms, "tflops": bwd_flops / (bwd_kernel_ms * 1e-3) / 1e12}},
+            "algorithmic": "F_fwd = 4*D*attended pairs per launch (blocks.hpp:191); bwd = 2.5*F_fwd"}
+    if N > 1:
+        # compute-or-NVLink roofline
+        send_b, recv_b = bundle.bwd_bytes()
+        B = [max(int(bundle.per_device_send[d]) + int(send_b[d]), int(bundle.per_device_recv[d]) + int(recv_b[d]))
+             for d in range(N)]
+        Fd = [3.5 * int(x) for x in bundle.dev_flops]
+        t_roof = max(max(Fd) / (pk["bf16_tflops"] * 1e12), max(B) / 900e9)
+        roof["plan_roofline_ms"] = t_roof * 1e3
+        roof["plan_roofline_frac"] = t_roof * 1e3 / ms_step
+
+    # end to end through the C ABI with host buffers (pinned), H2D + D2H inside the timed region
+    e2e = None
+    if not args.no_e2e:
+        hq, hk, hv, hdo = (x.cpu().pin_memory() for x in (q, k, v, d_o))
+        hdq, hdk, hdv = (torch.empty(x.shape, dtype=x.dtype).pin_memory() for x in (q, k, v))
+        def e2e_step():
+            ex.load_inputs(hq, hk, hv)
+            ex.forward(o, lse)
+            ex.backward(hdo, hdq, hdk, hdv, host=True)
+        for _ in range(2):
+            e2e_step()
+        ex.synchronize()
+        t0 = time.perf_counter()
+        ne = max(2, args.steps // 2)
+        for _ in range(ne):
+            e2e_step()
+        ex.synchronize()
+        e_ms = (time.perf_counter() - t0) / ne * 1e3
+        e2e = {"value": F_total / (e_ms * 1e-3) / 1e12, "unit": "TFLOP/s", "ms_per_step": e_ms,
+               "h2d_bytes_per_step": int(sum(x.numel() * 2 for x in (hq, hk, hv, hdo))),
+               "d2h_bytes_per_step": int(sum(x.numel() * 2 for x in (hdq, hdk, hdv))),
+               "path": "dcpx_load_inputs_host + dcpx_forward + dcpx_backward_host (pinned host buffers)"}
+
+    cb = None
+    if not args.no_cpu_baseline and N == 1:
+        try:
+            cb = cpu_baseline(bundle)
+            if cb:
+                cb = {k2: cb[k2] for k2 in ("value", "unit", "cores", "kind", "sample")}
+        except Exception as e:  # noqa: BLE001
+            cb = {"value": None, "unit": "TFLOP/s", "cores": 0, "kind": "reference", "sample": f"failed: {e}"}
+
+    line = {"metric": metric, "value": value, "unit": "TFLOP/s", "n_gpus": N, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": config, "roofline": roof, "cpu_baseline": cb, "e2e": e2e,
+            "gpu_launches": launches, "clocks": clk.summary(),
+            "detail": {"fwd_ms": sum(fwd_ms) / len(fwd_ms), "bwd_ms": sum(bwd_ms) / len(bwd_ms),
+                       "F_fwd": F_fwd, "F_total": F_total, "wall_ms_per_step": wall / args.steps * 1e3,
+                       "planned_fwd_bytes": int(bundle.volume[0])}}
+    print(json.dumps(line), flush=True)
+    ex.close()
+
+
+if __name__ == "__main__":
+    main()

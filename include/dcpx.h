@@ -153,7 +153,8 @@ typedef struct {
   double makespan;                   /* modeled, detail::cost_from_tables (schedule.hpp:217-236) */
   double device_ms;                  /* measured device time of the last call (max over devices) */
   int32_t kernel_launches;           /* executor kernels launched by the last call */
-  int32_t _pad;
+  int32_t attn_launches;             /* attention kernel (K1 / K1b) launches of the last call */
+  double attn_ms;                    /* summed device time of those launches (option "kernel_timing") */
 } dcpx_report;
 
 typedef struct dcpx_ctx dcpx_ctx;

@@ -224,3 +224,17 @@ def ref_time_tiles(count, nq, nk, D, rows, threads):
     if rc:
         raise RuntimeError(ref().dcpr_last_error().decode())
     return sec.value
+
+
+def ref_time_items(nq, nk, row_off, rows, D, threads):
+    """Reference exec_attention over sampled items (CPU baseline). Returns seconds."""
+    nq = np.ascontiguousarray(nq, np.int32)
+    nk = np.ascontiguousarray(nk, np.int32)
+    row_off = np.ascontiguousarray(row_off, np.int64)
+    rows = np.ascontiguousarray(rows, np.int32)
+    sec = C.c_double()
+    rc = ref().dcpr_time_items(len(nq), _p(nq), _p(nk), _p(row_off), _p(rows), D, threads,
+                               C.byref(sec))
+    if rc:
+        raise RuntimeError(ref().dcpr_last_error().decode())
+    return sec.value

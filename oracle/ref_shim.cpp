@@ -290,4 +290,46 @@ int dcpr_time_tiles(int count, int nq, int nk, int D, const int32_t* rows, int t
   }
 }
 
+// CPU baseline over a sample of real AttentionItems: item i has nq[i] x nk[i] tiles and
+// rows at rows + 4 * row_off[i] (kv-tile-relative, as compile_plans builds them).
+// exec_attention (simexec.hpp:33-76) runs on `threads` host threads, inputs N(0,1).
+int dcpr_time_items(int n, const int32_t* nq, const int32_t* nk, const int64_t* row_off,
+                    const int32_t* rows, int D, int threads, double* seconds) {
+  try {
+    int maxq = 1, maxk = 1;
+    for (int i = 0; i < n; ++i) { maxq = std::max(maxq, nq[i]); maxk = std::max(maxk, nk[i]); }
+    std::mt19937_64 rng(7);
+    std::normal_distribution<double> dist(0.0, 1.0);
+    dcp::Matrix q(maxq, D), k(maxk, D), v(maxk, D);
+    for (auto* m : {&q, &k, &v})
+      for (auto& x : m->a) x = dist(rng);
+    std::vector<dcp::Matrix> qs, ks, vs;
+    std::vector<std::vector<dcp::TokenRanges>> rr;
+    for (int i = 0; i < n; ++i) {
+      dcp::Matrix a(nq[i], D), b(nk[i], D), c(nk[i], D);
+      std::copy(q.a.begin(), q.a.begin() + static_cast<size_t>(nq[i]) * D, a.a.begin());
+      std::copy(k.a.begin(), k.a.begin() + static_cast<size_t>(nk[i]) * D, b.a.begin());
+      std::copy(v.a.begin(), v.a.begin() + static_cast<size_t>(nk[i]) * D, c.a.begin());
+      qs.push_back(std::move(a)); ks.push_back(std::move(b)); vs.push_back(std::move(c));
+      rr.push_back(to_rows(rows + 4 * row_off[i], nq[i]));
+    }
+    std::atomic<int> next{0};
+    const auto t0 = std::chrono::steady_clock::now();
+    std::vector<std::thread> pool;
+    for (int t = 0; t < threads; ++t)
+      pool.emplace_back([&] {
+        int i;
+        while ((i = next.fetch_add(1)) < n) {
+          volatile double sink = dcp::exec_attention(qs[i], ks[i], vs[i], rr[i]).out.a[0];
+          (void)sink;
+        }
+      });
+    for (auto& th : pool) th.join();
+    *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
+}
+
 }  // extern "C"

@@ -267,7 +267,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         mbar_wait(&bars.dq_full, g & 1);
         tc_fence_after();
         float* dst = p.dq_acc + ((int64_t)S.q_row0 + r) * 128;
-        const bool ok = r < S.n_q;
+        const bool ok = r < S.n_q && !(p.debug_flags & 1);
 #pragma unroll 1
         for (int c = 0; c < 128; c += 32) {
           uint32_t v[32];

@@ -91,6 +91,8 @@ dcpx_status dcpx_set_option(dcpx_ctx* ctx, const char* key, int64_t value) {
     else if (k == "remap_copies") ex.opt.remap_copies = value != 0;
     else if (k == "check_rows") ex.opt.check_rows = value != 0;
     else if (k == "timing") ex.opt.timing = value != 0;
+    else if (k == "kernel_timing") ex.opt.kernel_timing = value != 0;
+    else if (k == "bwd_debug") ex.opt.bwd_debug = static_cast<int>(value);
     else throw dcpx::Failure(DCPX_ERROR, "unknown option " + k);
   });
 }

@@ -129,6 +129,7 @@ Executor::~Executor() {
   for (auto& d : dev_) {
     DeviceGuard g(d.ordinal);
     for (auto e : d.events) cudaEventDestroy(e);
+    for (auto& e : d.kev) { cudaEventDestroy(e.first); cudaEventDestroy(e.second); }
     if (d.t0) cudaEventDestroy(d.t0);
     if (d.t1) cudaEventDestroy(d.t1);
     if (d.cs) cudaStreamDestroy(d.cs);
@@ -196,6 +197,18 @@ cudaEvent_t Executor::event(int d) {
     D.events.push_back(e);
   }
   return D.events[D.next_event++];
+}
+
+std::pair<cudaEvent_t, cudaEvent_t> Executor::kernel_events(int d) {
+  auto& D = dev_[d];
+  if (D.next_kev == D.kev.size()) {
+    DeviceGuard g(D.ordinal);
+    cudaEvent_t a, b;
+    CUDA_OK(cudaEventCreate(&a));
+    CUDA_OK(cudaEventCreate(&b));
+    D.kev.push_back({a, b});
+  }
+  return D.kev[D.next_kev++];
 }
 
 // ------------------------------------------------------------------------ prepare
@@ -1137,6 +1150,7 @@ void Executor::forward(void* o_out, float* lse_out, dcpx_report* rep, bool host)
   const int64_t TT = g_.total_tokens();
   for (auto& D : dev_) {
     D.next_event = 0;
+    D.next_kev = 0;
     D.launches = 0;
     DeviceGuard gd(D.ordinal);
     if (opt.timing) CUDA_OK(cudaEventRecord(D.t0, D.cs));
@@ -1154,7 +1168,10 @@ void Executor::forward(void* o_out, float* lse_out, dcpx_report* rep, bool host)
         p.o_arena = D.o; p.lse_arena = D.lse; p.num_units = op.num_units;
         p.slot_rows = static_cast<int32_t>(D.slot_rows);
         p.scale_log2 = static_cast<float>(1.4426950408889634 / std::sqrt(static_cast<double>(g_.D)));
+        std::pair<cudaEvent_t, cudaEvent_t> ke{};
+        if (opt.kernel_timing) { ke = kernel_events(d); CUDA_OK(cudaEventRecord(ke.first, D.cs)); }
         launch_attn_fwd(D.tm_q, D.tm_kv, p, op.grid, D.cs);
+        if (opt.kernel_timing) CUDA_OK(cudaEventRecord(ke.second, D.cs));
         ++D.launches;
         break;
       }
@@ -1262,6 +1279,22 @@ void Executor::fill_report(dcpx_report* rep, bool bwd) {
   }
   rep->wire_bytes = rep->total_bytes;
   for (int d = 0; d < R_; ++d) rep->kernel_launches += dev_[d].launches;
+  if (opt.kernel_timing) {
+    double mx = 0;
+    for (auto& D : dev_) {
+      DeviceGuard gd(D.ordinal);
+      double sum = 0;
+      for (size_t k = 0; k < D.next_kev; ++k) {
+        CUDA_OK(cudaEventSynchronize(D.kev[k].second));
+        float ms = 0;
+        CUDA_OK(cudaEventElapsedTime(&ms, D.kev[k].first, D.kev[k].second));
+        sum += ms;
+      }
+      rep->attn_launches += static_cast<int32_t>(D.next_kev);
+      mx = std::max(mx, sum);
+    }
+    rep->attn_ms = mx;
+  }
   if (opt.timing) {
     double mx = 0;
     for (auto& D : dev_) {
@@ -1285,6 +1318,7 @@ void Executor::backward(const void* d_o, void* dq, void* dk, void* dv, dcpx_repo
   const size_t bq = TT * H * 256, bk = TT * G * 256;
   for (auto& D : dev_) {
     D.next_event = 0;
+    D.next_kev = 0;
     D.launches = 0;
     DeviceGuard gd(D.ordinal);
     if (opt.timing) CUDA_OK(cudaEventRecord(D.t0, D.cs));
@@ -1347,7 +1381,11 @@ void Executor::backward(const void* d_o, void* dq, void* dk, void* dv, dcpx_repo
           p.slot_rows = static_cast<int32_t>(D.slot_rows);
           p.scale_log2 = static_cast<float>(1.4426950408889634) * scale;
           p.scale = scale;
+          p.debug_flags = opt.bwd_debug;
+          std::pair<cudaEvent_t, cudaEvent_t> ke{};
+          if (opt.kernel_timing) { ke = kernel_events(d); CUDA_OK(cudaEventRecord(ke.first, D.cs)); }
           launch_attn_bwd(D.tm_q, D.tm_do, D.tm_kv, p, op.bgrid, D.cs);
+          if (opt.kernel_timing) CUDA_OK(cudaEventRecord(ke.second, D.cs));
           ++D.launches;
         }
         if (op.ret.dj.n_blocks) {

@@ -106,6 +106,8 @@ struct DevState {
   size_t next_event = 0;
   cudaEvent_t t0 = nullptr, t1 = nullptr;
   int launches = 0;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> kev;  // per attention launch (kernel_timing)
+  size_t next_kev = 0;
 };
 
 struct Options {
@@ -113,6 +115,8 @@ struct Options {
   bool remap_copies = true;
   bool check_rows = false;
   bool timing = true;
+  int bwd_debug = 0;
+  bool kernel_timing = false;
 };
 
 class Executor {
@@ -137,6 +141,7 @@ class Executor {
   void fill_report(dcpx_report* rep, bool bwd);
   void simulate_order();
   cudaEvent_t event(int d);
+  std::pair<cudaEvent_t, cudaEvent_t> kernel_events(int d);
   void free_all();
 
   int R_ = 0;

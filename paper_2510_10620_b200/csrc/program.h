@@ -96,6 +96,8 @@ struct BwdParams {
   int32_t slot_rows;
   float scale_log2;
   float scale;
+  int32_t debug_flags;  // bit0: skip the dQ reduce-add (timing experiments only)
+  int32_t _pad;
 };
 
 struct FwdParams {

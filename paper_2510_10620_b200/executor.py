@@ -82,7 +82,8 @@ def _report_dict(r: P.c_report) -> dict:
     return dict(devices=n, stages=r.stages, total_bytes=int(r.total_bytes),
                 total_flops=int(r.total_flops), per_device_send=[int(x) for x in r.per_device_send[:n]],
                 per_device_recv=[int(x) for x in r.per_device_recv[:n]], wire_bytes=int(r.wire_bytes),
-                makespan=r.makespan, device_ms=r.device_ms, kernel_launches=r.kernel_launches)
+                makespan=r.makespan, device_ms=r.device_ms, kernel_launches=r.kernel_launches,
+                attn_launches=r.attn_launches, attn_ms=r.attn_ms)
 
 
 def _ptr(t) -> Optional[int]:

@@ -76,7 +76,8 @@ class c_report(C.Structure):
                 ("total_flops", C.c_uint64), ("per_device_send", C.c_uint64 * 64),
                 ("per_device_recv", C.c_uint64 * 64), ("wire_bytes", C.c_uint64),
                 ("makespan", C.c_double), ("device_ms", C.c_double),
-                ("kernel_launches", C.c_int32), ("_pad", C.c_int32)]
+                ("kernel_launches", C.c_int32), ("attn_launches", C.c_int32),
+                ("attn_ms", C.c_double)]
 
 
 def _ptr(a: np.ndarray) -> int:

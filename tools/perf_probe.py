@@ -24,6 +24,8 @@ def main():
     v = torch.randn((T, G, 128), device="cuda", generator=g).to(torch.bfloat16)
     ex = DCPExecutor([0] * b.R)
     ex.prepare(b)
+    if len(sys.argv) > 3:
+        ex.set_option('bwd_debug', int(sys.argv[3]))
     o = torch.empty((T, H, 128), dtype=torch.bfloat16, device="cuda")
     lse = torch.empty((H, T), device="cuda")
     ex.load_inputs(q, k, v)
@@ -36,6 +38,21 @@ def main():
     ms = min(times)
     print(f"{name}: fwd flops {b.total_flops / 1e12:.3f} T  device {ms:.3f} ms (median {sorted(times)[len(times)//2]:.3f})"
           f"  -> {b.total_flops / ms / 1e9:.1f} TFLOP/s  launches {rep['kernel_launches']}")
+    d_o = torch.randn((T, H, 128), device="cuda", generator=g).to(torch.bfloat16)
+    dq = torch.empty_like(q)
+    dk = torch.empty_like(k)
+    dv = torch.empty_like(v)
+    bt = []
+    for _ in range(3):
+        ex.forward(o, lse)
+        ex.backward(d_o, dq, dk, dv)
+    for _ in range(iters):
+        ex.forward(o, lse)
+        rep = ex.backward(d_o, dq, dk, dv)
+        bt.append(rep["device_ms"])
+    bms = min(bt)
+    print(f"{name}: bwd flops {rep['total_flops'] / 1e12:.3f} T  device {bms:.3f} ms -> {rep['total_flops'] / bms / 1e9:.1f} TFLOP/s;"
+          f"  fwd+bwd {ms + bms:.3f} ms -> {3.5 * b.total_flops / (ms + bms) / 1e9:.1f} TFLOP/s")
 
 
 if __name__ == "__main__":
