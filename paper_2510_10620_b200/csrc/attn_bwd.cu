@@ -12,10 +12,16 @@
 // CTA = 384 threads, persistent:
 //   warp 0      TMA producer: K, V per unit; Q, dO tiles + LSE/Delta rows per step (2 stages)
 //   warp 1      TMEM owner + tcgen05.mma issuer
-//   warps 4-7   P / dS: thread = kv row (TMEM lane); P^T -> TMEM, dS^T -> smem (SW128)
-//   warps 8-11  dQ drain (TMEM -> red.global.add.v4.f32) and the dK epilogue
+//   warps 2-3   idle (register donors)
+//   warps 4-11  compute: warp group c = 0/1 handles q columns [64c, 64c+64) of every kv row
+//               (TMEM lane = kv row): P^T -> TMEM, dS^T -> smem (SW128); then drain the dQ
+//               columns [64c, 64c+64) of every q row with red.global.add.v4.f32; at the end
+//               of a unit group 0 adds dV and group 1 adds dK to the fp32 accumulators.
 // TMEM: S^T [0,128) (P^T bf16 overwrites [0,64)), dP^T [128,256) (reused for dQ),
 //       dV [256,384), dK [384,512).
+// Masks: for partial tiles each lane builds 32-bit words "q row -> kv rows of my warp"
+// from the q rows' <= 2 attend ranges and transposes them across the warp (5 shuffles),
+// giving every kv-row thread a bitmask over its q columns; the element loop is branch-free.
 #include <cuda_bf16.h>
 #include <math_constants.h>
 
@@ -36,14 +42,33 @@ struct BwdBarriers {
   uint32_t tmem_base;
 };
 
-__device__ __forceinline__ uint32_t bwd_cls(uint32_t c) { return c & 3u; }
-
 // fp32 vector reduce-add into global memory (accumulators are shared with other CTAs
 // and with peer devices' gradient returns, so every update is atomic).
 __device__ __forceinline__ void red_add_v4(float* dst, const uint32_t* v) {
   asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst), "f"(__uint_as_float(v[0])),
                "f"(__uint_as_float(v[1])), "f"(__uint_as_float(v[2])), "f"(__uint_as_float(v[3]))
                : "memory");
+}
+
+// Bits [a, b) of a 32-bit word (a, b may lie outside [0, 32]).
+__device__ __forceinline__ uint32_t bits_in(int64_t a, int64_t b) {
+  a = a < 0 ? 0 : a;
+  b = b > 32 ? 32 : b;
+  if (b <= a) return 0u;
+  const uint32_t hi = b == 32 ? 0xffffffffu : ((1u << b) - 1u);
+  return hi & ~((1u << a) - 1u);
+}
+
+// 32x32 bit-matrix transpose across a warp: lane i holds row i (bit j = column j); on
+// return lane j holds column j (bit i = row i).
+__device__ __forceinline__ uint32_t warp_transpose32(uint32_t x, int lane) {
+#pragma unroll
+  for (int s = 16; s >= 1; s >>= 1) {
+    const uint32_t m = s == 16 ? 0x0000ffffu : s == 8 ? 0x00ff00ffu : s == 4 ? 0x0f0f0f0fu : s == 2 ? 0x33333333u : 0x55555555u;
+    const uint32_t y = __shfl_xor_sync(0xffffffffu, x, s);
+    x = (lane & s) ? ((x & ~m) | ((y & ~m) >> s)) : ((x & m) | ((y & m) << s));
+  }
+  return x;
 }
 
 __global__ void __launch_bounds__(kBwdThreads, 1)
@@ -71,9 +96,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       mbar_init(&bars.q_empty[i], 1);
     }
     mbar_init(&bars.s_full, 1);
-    mbar_init(&bars.p_ready, 128);
+    mbar_init(&bars.p_ready, 256);
     mbar_init(&bars.dq_full, 1);
-    mbar_init(&bars.dq_empty, 128);
+    mbar_init(&bars.dq_empty, 256);
     mbar_init(&bars.ds_free, 1);
     mbar_init(&bars.acc_full, 1);
     mbar_init(&bars.acc_empty, 256);
@@ -177,11 +202,13 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         umma_commit(&bars.kv_empty);
       }
     }
-  } else if (warp >= 4 && warp < 8) {
-    // ------------------------------------------------------------ P / dS (thread = kv row)
+  } else if (warp >= 4) {
+    // ------------------------------------------------------------ compute warps
     asm volatile("setmaxnreg.inc.sync.aligned.u32 208;");
-    const int j = ((warp & 3) << 5) + lane;
-    const uint32_t lane_addr = tbase + ((uint32_t)((warp & 3) * 32) << 16);
+    const int c = (warp - 4) >> 2;                  // q-column half handled by this group
+    const int wq = warp & 3;                        // TMEM lane quarter
+    const int j = (wq << 5) + lane;                 // kv row (P/dS) / q row (dQ drain)
+    const uint32_t lane_addr = tbase + ((uint32_t)(wq * 32) << 16);
     uint32_t g = 0, it = 0;
     for (int u = blockIdx.x; u < p.num_units; u += gridDim.x, ++it) {
       const BwdUnit U = p.units[u];
@@ -189,45 +216,71 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       for (int s = 0; s < U.step_count; ++s, ++g) {
         const BwdStep S = p.steps[U.step_begin + s];
         const int st = g & 1;
-        const uint32_t cl = bwd_cls(S.cls);
-        const ItemMask im = p.items[S.item];
-        const int64_t kvrel = (int64_t)S.col0 + j + im.kv_shift;  // in range coordinates
+        // ---- mask bits over my 64 q columns: mb[h] bit i <-> q column 64c + 32h + i
+        uint32_t mb[2];
+        if (S.cls == kTilePartial) {
+          const ItemMask im = p.items[S.item];
+          const int64_t base = im.kv_shift + S.col0 + 32 * wq;  // range coords of my warp's kv row 0
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int qi = 64 * c + 32 * h + lane;           // q row this lane describes
+            uint32_t w = 0u;
+            if (qi < S.n_q) {
+              const int4 rg = __ldg(reinterpret_cast<const int4*>(p.ranges) + im.range_row0 + S.q_local0 + qi);
+              w = bits_in((int64_t)rg.x - base, (int64_t)rg.y - base) | bits_in((int64_t)rg.z - base, (int64_t)rg.w - base);
+            }
+            mb[h] = warp_transpose32(w, lane);
+          }
+        } else {
+#pragma unroll
+          for (int h = 0; h < 2; ++h) mb[h] = bits_in(0, S.n_q - 64 * c - 32 * h);
+        }
+        if (!kv_valid) mb[0] = mb[1] = 0u;
         mbar_wait(&bars.s_full, g & 1);
         tc_fence_after();
         if (g > 0) mbar_wait(&bars.ds_free, (g - 1) & 1);
-        const float* lse2 = sLSE + st * 128;
-        const float* dlt = sDelta + st * 128;
-#pragma unroll 1
-        for (int c = 0; c < 128; c += 32) {
-          uint32_t sr[32], dr[32];
-          tmem_ld32(lane_addr + c, sr);
-          tmem_ld32(lane_addr + 128 + c, dr);
+        const float4* lse4 = reinterpret_cast<const float4*>(sLSE + st * 128 + 64 * c);
+        const float4* dlt4 = reinterpret_cast<const float4*>(sDelta + st * 128 + 64 * c);
+        // P^T (bf16) lands in S^T columns [0,64): every S^T column must be read by both
+        // groups before either group stores P.
+        uint32_t srr[2][32];
+        tmem_ld32(lane_addr + 64 * c, srr[0]);
+        tmem_ld32(lane_addr + 64 * c + 32, srr[1]);
+        tmem_wait_ld();
+        named_bar_sync(1, 256);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int col = 64 * c + 32 * h;  // first q column of this chunk
+          const uint32_t* sr = srr[h];
+          uint32_t dr[32];
+          tmem_ld32(lane_addr + 128 + col, dr);
           tmem_wait_ld();
           uint32_t pk[16], dk[16];
 #pragma unroll
-          for (int e = 0; e < 16; ++e) {
-            float pv[2], dv[2];
+          for (int e4 = 0; e4 < 8; ++e4) {
+            const float4 l4 = lse4[8 * h + e4];
+            const float4 d4 = dlt4[8 * h + e4];
+            const float lv[4] = {l4.x, l4.y, l4.z, l4.w};
+            const float dv[4] = {d4.x, d4.y, d4.z, d4.w};
+            float pv[4], sv[4];
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
-              const int i = c + 2 * e + h;
-              bool ok = kv_valid && i < S.n_q;
-              if (ok && cl == kTilePartial) {
-                const int4 rg = __ldg(reinterpret_cast<const int4*>(p.ranges) + im.range_row0 + S.q_local0 + i);
-                ok = (kvrel >= rg.x && kvrel < rg.y) || (kvrel >= rg.z && kvrel < rg.w);
-              }
-              const float pe = ok ? fast_exp2(fmaf(__uint_as_float(sr[2 * e + h]), p.scale_log2, -lse2[i])) : 0.f;
-              pv[h] = pe;
-              dv[h] = pe * (__uint_as_float(dr[2 * e + h]) - dlt[i]) * p.scale;
+            for (int e = 0; e < 4; ++e) {
+              const int i = 4 * e4 + e;
+              const float pe = fast_exp2(fmaf(__uint_as_float(sr[i]), p.scale_log2, -lv[e]));
+              pv[e] = ((mb[h] >> i) & 1u) ? pe : 0.f;
+              sv[e] = pv[e] * (__uint_as_float(dr[i]) - dv[e]) * p.scale;
             }
-            pk[e] = pack_bf16(pv[0], pv[1]);
-            dk[e] = pack_bf16(dv[0], dv[1]);
+            pk[2 * e4] = pack_bf16(pv[0], pv[1]);
+            pk[2 * e4 + 1] = pack_bf16(pv[2], pv[3]);
+            dk[2 * e4] = pack_bf16(sv[0], sv[1]);
+            dk[2 * e4 + 1] = pack_bf16(sv[2], sv[3]);
           }
-          tmem_st16(lane_addr + (c >> 1), pk);
-          // dS^T row j, q columns [c, c+32): 4 chunks of 16 B, 128B-swizzled
-          uint8_t* row = sDS + (c >> 6) * 16384 + j * 128;
+          tmem_st16(lane_addr + (col >> 1), pk);
+          // dS^T row j, q columns [col, col+32): 4 chunks of 16 B in half c, 128B-swizzled
+          uint8_t* row = sDS + c * 16384 + j * 128;
 #pragma unroll
           for (int q4 = 0; q4 < 4; ++q4) {
-            const int chunk = ((c & 63) >> 3) + q4;
+            const int chunk = 4 * h + q4;
             *reinterpret_cast<uint4*>(row + ((chunk ^ (j & 7)) << 4)) =
                 make_uint4(dk[4 * q4], dk[4 * q4 + 1], dk[4 * q4 + 2], dk[4 * q4 + 3]);
           }
@@ -236,63 +289,39 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         fence_proxy_async_smem();
         tc_fence_before();
         mbar_arrive(&bars.p_ready);
-      }
-      // dV epilogue: dV acc [256,384) -> dKV accumulator (fp32, V half of the slot)
-      mbar_wait(&bars.acc_full, it & 1);
-      tc_fence_after();
-      float* dst = p.dkv_acc + ((int64_t)U.kv_row0 + p.slot_rows + j) * 128;
-#pragma unroll 1
-      for (int c = 0; c < 128; c += 32) {
-        uint32_t r[32];
-        tmem_ld32(lane_addr + 256 + c, r);
-        tmem_wait_ld();
-        if (kv_valid) {
-#pragma unroll
-          for (int e = 0; e < 32; e += 4) red_add_v4(dst + c + e, r + e);
-        }
-      }
-      tc_fence_before();
-      mbar_arrive(&bars.acc_empty);
-    }
-  } else if (warp >= 8) {
-    // ------------------------------------------------------------ dQ drain + dK epilogue
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 208;");
-    const int r = ((warp & 3) << 5) + lane;  // q row of the step / kv row of the unit
-    const uint32_t lane_addr = tbase + ((uint32_t)((warp & 3) * 32) << 16);
-    uint32_t g = 0, it = 0;
-    for (int u = blockIdx.x; u < p.num_units; u += gridDim.x, ++it) {
-      const BwdUnit U = p.units[u];
-      for (int s = 0; s < U.step_count; ++s, ++g) {
-        const BwdStep S = p.steps[U.step_begin + s];
+        // ---- dQ drain: q row j, columns [64c, 64c+64) of dQ (TMEM cols [128,256))
         mbar_wait(&bars.dq_full, g & 1);
         tc_fence_after();
-        float* dst = p.dq_acc + ((int64_t)S.q_row0 + r) * 128;
-        const bool ok = r < S.n_q && !(p.debug_flags & 1);
-#pragma unroll 1
-        for (int c = 0; c < 128; c += 32) {
-          uint32_t v[32];
-          tmem_ld32(lane_addr + 128 + c, v);
+        {
+          float* dst = p.dq_acc + ((int64_t)S.q_row0 + j) * 128 + 64 * c;
+          const bool ok = j < S.n_q && !(p.debug_flags & 1);
+          uint32_t v0[32], v1[32];
+          tmem_ld32(lane_addr + 128 + 64 * c, v0);
+          tmem_ld32(lane_addr + 128 + 64 * c + 32, v1);
           tmem_wait_ld();
+          tc_fence_before();
+          mbar_arrive(&bars.dq_empty);
           if (ok) {
 #pragma unroll
-            for (int e = 0; e < 32; e += 4) red_add_v4(dst + c + e, v + e);
+            for (int e = 0; e < 32; e += 4) red_add_v4(dst + e, v0 + e);
+#pragma unroll
+            for (int e = 0; e < 32; e += 4) red_add_v4(dst + 32 + e, v1 + e);
           }
         }
-        tc_fence_before();
-        mbar_arrive(&bars.dq_empty);
       }
+      // ---- unit epilogue: group 0 adds dV [256,384), group 1 adds dK [384,512)
       mbar_wait(&bars.acc_full, it & 1);
       tc_fence_after();
-      float* dst = p.dkv_acc + ((int64_t)U.kv_row0 + r) * 128;
-      const bool kv_valid = r < U.n_kv;
+      float* dst = p.dkv_acc + ((int64_t)U.kv_row0 + (c == 0 ? p.slot_rows : 0) + j) * 128;
+      const uint32_t col = c == 0 ? 256 : 384;
 #pragma unroll 1
-      for (int c = 0; c < 128; c += 32) {
-        uint32_t v[32];
-        tmem_ld32(lane_addr + 384 + c, v);
+      for (int cc = 0; cc < 128; cc += 32) {
+        uint32_t r[32];
+        tmem_ld32(lane_addr + col + cc, r);
         tmem_wait_ld();
         if (kv_valid) {
 #pragma unroll
-          for (int e = 0; e < 32; e += 4) red_add_v4(dst + c + e, v + e);
+          for (int e = 0; e < 32; e += 4) red_add_v4(dst + cc + e, r + e);
         }
       }
       tc_fence_before();
