@@ -15,8 +15,9 @@
 //   warps 2-3   idle (register donors)
 //   warps 4-11  compute: warp group c = 0/1 handles q columns [64c, 64c+64) of every kv row
 //               (TMEM lane = kv row): P^T -> TMEM, dS^T -> smem (SW128); then drain the dQ
-//               columns [64c, 64c+64) of every q row with red.global.add.v4.f32; at the end
-//               of a unit group 0 adds dV and group 1 adds dK to the fp32 accumulators.
+//               columns [64c, 64c+64) of every q row: TMEM -> smem (fp32, SW128) -> TMA
+//               bulk-tensor reduce-add into the dQ accumulator; at the end of a unit
+//               group 0 adds dV and group 1 adds dK to the fp32 accumulators.
 // TMEM: S^T [0,128) (P^T bf16 overwrites [0,64)), dP^T [128,256) (reused for dQ),
 //       dV [256,384), dK [384,512).
 // Masks: for partial tiles each lane builds 32-bit words "q row -> kv rows of my warp"
@@ -73,7 +74,8 @@ __device__ __forceinline__ uint32_t warp_transpose32(uint32_t x, int lane) {
 
 __global__ void __launch_bounds__(kBwdThreads, 1)
     attn_bwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_do,
-                    const __grid_constant__ CUtensorMap tm_kv, const BwdParams p) {
+                    const __grid_constant__ CUtensorMap tm_kv, const __grid_constant__ CUtensorMap tm_dq,
+                    const BwdParams p) {
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* sK = smem;
   uint8_t* sV = smem + 32768;
@@ -106,6 +108,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     tma_prefetch_desc(&tm_q);
     tma_prefetch_desc(&tm_do);
     tma_prefetch_desc(&tm_kv);
+    tma_prefetch_desc(&tm_dq);
   }
   if (warp == 1) tmem_alloc<512>(&bars.tmem_base);
   tc_fence_before();
@@ -213,13 +216,20 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     for (int u = blockIdx.x; u < p.num_units; u += gridDim.x, ++it) {
       const BwdUnit U = p.units[u];
       const bool kv_valid = j < U.n_kv;
+      // step descriptors are loaded one step ahead so their latency hides behind the work
+      BwdStep s_next = p.steps[U.step_begin];
+      ItemMask m_next = p.items[s_next.item];
       for (int s = 0; s < U.step_count; ++s, ++g) {
-        const BwdStep S = p.steps[U.step_begin + s];
+        const BwdStep S = s_next;
+        const ItemMask im = m_next;
+        if (s + 1 < U.step_count) {
+          s_next = p.steps[U.step_begin + s + 1];
+          m_next = p.items[s_next.item];
+        }
         const int st = g & 1;
         // ---- mask bits over my 64 q columns: mb[h] bit i <-> q column 64c + 32h + i
         uint32_t mb[2];
         if (S.cls == kTilePartial) {
-          const ItemMask im = p.items[S.item];
           const int64_t base = im.kv_shift + S.col0 + 32 * wq;  // range coords of my warp's kv row 0
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
@@ -289,23 +299,36 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         fence_proxy_async_smem();
         tc_fence_before();
         mbar_arrive(&bars.p_ready);
-        // ---- dQ drain: q row j, columns [64c, 64c+64) of dQ (TMEM cols [128,256))
+        // ---- dQ drain: q row j, columns [64c, 64c+64) of dQ (TMEM cols [128,256)).
+        // Staged as two [128 rows x 32 cols] fp32 chunks (128B-swizzled) through this
+        // group's own 16 KiB half of the dS buffer (free once dQ's MMA retired) and
+        // reduce-added into the dQ accumulator by one TMA bulk-tensor op per chunk.
         mbar_wait(&bars.dq_full, g & 1);
         tc_fence_after();
         {
-          float* dst = p.dq_acc + ((int64_t)S.q_row0 + j) * 128 + 64 * c;
-          const bool ok = j < S.n_q && !(p.debug_flags & 1);
           uint32_t v0[32], v1[32];
           tmem_ld32(lane_addr + 128 + 64 * c, v0);
           tmem_ld32(lane_addr + 128 + 64 * c + 32, v1);
           tmem_wait_ld();
           tc_fence_before();
           mbar_arrive(&bars.dq_empty);
-          if (ok) {
+          uint8_t* stage = sDS + c * 16384;
 #pragma unroll
-            for (int e = 0; e < 32; e += 4) red_add_v4(dst + e, v0 + e);
+          for (int r = 0; r < 2; ++r) {
+            const uint32_t* v = r ? v1 : v0;
+            uint8_t* row = stage + j * 128;
 #pragma unroll
-            for (int e = 0; e < 32; e += 4) red_add_v4(dst + 32 + e, v1 + e);
+            for (int q4 = 0; q4 < 8; ++q4)
+              *reinterpret_cast<uint4*>(row + ((q4 ^ (j & 7)) << 4)) =
+                  make_uint4(v[4 * q4], v[4 * q4 + 1], v[4 * q4 + 2], v[4 * q4 + 3]);
+            fence_proxy_async_smem();
+            named_bar_sync(2 + c, 128);
+            if (wq == 0 && lane == 0 && !(p.debug_flags & 1)) {
+              tma_reduce_add_2d(&tm_dq, stage, 64 * c + 32 * r, S.q_row0);
+              bulk_commit();
+              bulk_wait_read<0>();
+            }
+            named_bar_sync(2 + c, 128);
           }
         }
       }
@@ -334,13 +357,13 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 }
 
 void launch_attn_bwd(const CUtensorMap& tm_q, const CUtensorMap& tm_do, const CUtensorMap& tm_kv,
-                     const BwdParams& p, int grid, cudaStream_t stream) {
+                     const CUtensorMap& tm_dq, const BwdParams& p, int grid, cudaStream_t stream) {
   static bool configured = false;
   if (!configured) {
     cudaFuncSetAttribute(attn_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kBwdSmem);
     configured = true;
   }
-  attn_bwd_kernel<<<grid, kBwdThreads, kBwdSmem, stream>>>(tm_q, tm_do, tm_kv, p);
+  attn_bwd_kernel<<<grid, kBwdThreads, kBwdSmem, stream>>>(tm_q, tm_do, tm_kv, tm_dq, p);
 }
 
 }  // namespace dcpx

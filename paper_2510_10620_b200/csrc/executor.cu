@@ -74,6 +74,21 @@ CUtensorMap make_tmap(void* base, int64_t rows) {
   return m;
 }
 
+// 2-D fp32 tensor map over a [rows][128] accumulator, box 128 rows x 32 columns (128 B),
+// 128-byte swizzle: the TMA reduce-add target of the backward's dQ drain.
+CUtensorMap make_tmap_f32(void* base, int64_t rows) {
+  CUtensorMap m;
+  cuuint64_t dims[2] = {128, static_cast<cuuint64_t>(rows)};
+  cuuint64_t strides[1] = {512};
+  cuuint32_t box[2] = {32, 128};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, base, dims, strides, box, es,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw Failure(DCPX_CUDA_ERROR, "cuTensorMapEncodeTiled (f32) failed: " + std::to_string(r));
+  return m;
+}
+
 int num_sms(int ordinal) {
   int n = 0;
   cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, ordinal);
@@ -699,6 +714,7 @@ void Executor::compile_device(int d) {
     CUDA_OK(cudaMemset(D.lse2, 0, nq * SR * 4));
     CUDA_OK(cudaMemset(D.delta, 0, nq * SR * 4));
     D.tm_do = make_tmap(D.d_o, nq * SR);
+    D.tm_dq = make_tmap_f32(D.dq_acc, nq * SR);
     D.tm_q = make_tmap(D.q, std::max<int64_t>(1, D.cap_q) * SR);
     D.tm_kv = make_tmap(D.kv, std::max<int64_t>(1, D.cap_kv) * 2 * SR);
     std::vector<int32_t> ranges = g_.ranges;
@@ -1384,7 +1400,7 @@ void Executor::backward(const void* d_o, void* dq, void* dk, void* dv, dcpx_repo
           p.debug_flags = opt.bwd_debug;
           std::pair<cudaEvent_t, cudaEvent_t> ke{};
           if (opt.kernel_timing) { ke = kernel_events(d); CUDA_OK(cudaEventRecord(ke.first, D.cs)); }
-          launch_attn_bwd(D.tm_q, D.tm_do, D.tm_kv, p, op.bgrid, D.cs);
+          launch_attn_bwd(D.tm_q, D.tm_do, D.tm_kv, D.tm_dq, p, op.bgrid, D.cs);
           if (opt.kernel_timing) CUDA_OK(cudaEventRecord(ke.second, D.cs));
           ++D.launches;
         }

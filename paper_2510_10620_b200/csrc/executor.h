@@ -99,7 +99,7 @@ struct DevState {
   // backward arenas (parallel to Q / KV arenas) and their io jobs
   __nv_bfloat16* d_o = nullptr;
   float *lse2 = nullptr, *delta = nullptr, *dq_acc = nullptr, *dkv_acc = nullptr;
-  CUtensorMap tm_do{};
+  CUtensorMap tm_do{}, tm_dq{};
   JobList scatter_do, prep, gather_dq, gather_dk, gather_dv;
   std::vector<int32_t> final_o_slot;  // per resident_o entry: physical slot holding the result
   std::vector<cudaEvent_t> events;

@@ -125,6 +125,13 @@ __device__ __forceinline__ void bulk_reduce_add_f32(float* gmem, const void* sme
       "r"(smem_u32(smem)), "r"(bytes)
       : "memory");
 }
+// 2-D tensor reduce-add (fp32) from shared memory into global memory through TMA.
+__device__ __forceinline__ void tma_reduce_add_2d(const void* desc, const void* smem, int32_t x, int32_t y) {
+  asm volatile(
+      "cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.bulk_group [%0, {%2, %3}], [%1];" ::"l"(desc),
+      "r"(smem_u32(smem)), "r"(x), "r"(y)
+      : "memory");
+}
 __device__ __forceinline__ void bulk_commit() {
   asm volatile("cp.async.bulk.commit_group;" ::: "memory");
 }
