@@ -236,7 +236,7 @@ def main():
         for _ in range(args.steps):
             rf, rb = step()
             fwd_ms.append(rf["device_ms"]); bwd_ms.append(rb["device_ms"])
-            fwd_k.append(rf["attn_ms"]); bwd_k.append(rb["attn_ms"])
+            fwd_k.append(rf["attn_ms_sum"]); bwd_k.append(rb["attn_ms_sum"])
             launches += rf["kernel_launches"] + rb["kernel_launches"] + 3 * N  # + q/k/v scatters
         for d in range(N):
             with torch.cuda.device(d):
@@ -250,7 +250,8 @@ def main():
     ms_step = max(total_ms / args.steps, (sum(fwd_ms) + sum(bwd_ms)) / args.steps)
     value = F_total / (ms_step * 1e-3) / 1e12
 
-    # roofline of the dominant kernel (backward attention, K1b) and of the forward (K1)
+    # roofline of the dominant kernel (backward attention, K1b) and of the forward (K1):
+    # algorithmic FLOPs of all launches / GPU-time summed over the devices' launches
     pk, src = peaks()
     peak = pk.get("bf16_tflops_sustained", pk["bf16_tflops"])
     bwd_kernel_ms = sum(bwd_k) / len(bwd_k)
@@ -271,8 +272,8 @@ def main():
     roof = {"bound": "tensor", "kernel": dominant, "achieved": ach, "peak": peak, "unit": "TFLOP/s",
             "frac": ach / peak, "traffic": traffic,
             "peak_source": f"{src} bf16_tflops_sustained (kernel timed inside a long step)",
-            "per_kernel": {"attn_fwd_kernel": {"ms": fwd_kernel_ms, "tflops": fwd_flops / (fwd_kernel_ms * 1e-3) / 1e12},
-                           "attn_bwd_kernel": {"ms": bwd_kernel_ms, "tflops": bwd_flops / (bwd_kernel_ms * 1e-3) / 1e12}},
+            "per_kernel": {"attn_fwd_kernel": {"gpu_ms": fwd_kernel_ms, "tflops": fwd_flops / (fwd_kernel_ms * 1e-3) / 1e12},
+                           "attn_bwd_kernel": {"gpu_ms": bwd_kernel_ms, "tflops": bwd_flops / (bwd_kernel_ms * 1e-3) / 1e12}},
             "algorithmic": "F_fwd = 4*D*attended pairs per launch (blocks.hpp:191); bwd = 2.5*F_fwd"}
     if N > 1:
         # compute-or-NVLink roofline

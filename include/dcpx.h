@@ -154,7 +154,8 @@ typedef struct {
   double device_ms;                  /* measured device time of the last call (max over devices) */
   int32_t kernel_launches;           /* executor kernels launched by the last call */
   int32_t attn_launches;             /* attention kernel (K1 / K1b) launches of the last call */
-  double attn_ms;                    /* summed device time of those launches (option "kernel_timing") */
+  double attn_ms;                    /* max over devices of the summed device time of those launches */
+  double attn_ms_sum;                /* the same summed over devices (GPU-time spent in the kernel) */
 } dcpx_report;
 
 typedef struct dcpx_ctx dcpx_ctx;

@@ -358,10 +358,13 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 
 void launch_attn_bwd(const CUtensorMap& tm_q, const CUtensorMap& tm_do, const CUtensorMap& tm_kv,
                      const CUtensorMap& tm_dq, const BwdParams& p, int grid, cudaStream_t stream) {
-  static bool configured = false;
-  if (!configured) {
+  // the dynamic shared-memory opt-in is a per-device function attribute
+  static uint64_t configured = 0;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!(configured & (1ull << dev))) {
     cudaFuncSetAttribute(attn_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kBwdSmem);
-    configured = true;
+    configured |= 1ull << dev;
   }
   attn_bwd_kernel<<<grid, kBwdThreads, kBwdSmem, stream>>>(tm_q, tm_do, tm_kv, tm_dq, p);
 }

@@ -365,10 +365,13 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
 
 void launch_attn_fwd(const CUtensorMap& tm_q, const CUtensorMap& tm_kv, const FwdParams& p,
                      int grid, cudaStream_t stream) {
-  static bool configured = false;
-  if (!configured) {
+  // the dynamic shared-memory opt-in is a per-device function attribute
+  static uint64_t configured = 0;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!(configured & (1ull << dev))) {
     cudaFuncSetAttribute(attn_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kFwdSmem);
-    configured = true;
+    configured |= 1ull << dev;
   }
   attn_fwd_kernel<<<grid, kFwdThreads, kFwdSmem, stream>>>(tm_q, tm_kv, p);
 }

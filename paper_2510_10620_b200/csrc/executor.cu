@@ -1307,6 +1307,7 @@ void Executor::fill_report(dcpx_report* rep, bool bwd) {
         sum += ms;
       }
       rep->attn_launches += static_cast<int32_t>(D.next_kev);
+      rep->attn_ms_sum += sum;
       mx = std::max(mx, sum);
     }
     rep->attn_ms = mx;

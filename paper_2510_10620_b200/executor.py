@@ -83,7 +83,7 @@ def _report_dict(r: P.c_report) -> dict:
                 total_flops=int(r.total_flops), per_device_send=[int(x) for x in r.per_device_send[:n]],
                 per_device_recv=[int(x) for x in r.per_device_recv[:n]], wire_bytes=int(r.wire_bytes),
                 makespan=r.makespan, device_ms=r.device_ms, kernel_launches=r.kernel_launches,
-                attn_launches=r.attn_launches, attn_ms=r.attn_ms)
+                attn_launches=r.attn_launches, attn_ms=r.attn_ms, attn_ms_sum=r.attn_ms_sum)
 
 
 def _ptr(t) -> Optional[int]:

@@ -77,7 +77,7 @@ class c_report(C.Structure):
                 ("per_device_recv", C.c_uint64 * 64), ("wire_bytes", C.c_uint64),
                 ("makespan", C.c_double), ("device_ms", C.c_double),
                 ("kernel_launches", C.c_int32), ("attn_launches", C.c_int32),
-                ("attn_ms", C.c_double)]
+                ("attn_ms", C.c_double), ("attn_ms_sum", C.c_double)]
 
 
 def _ptr(a: np.ndarray) -> int:

@@ -1,0 +1,47 @@
+"""GPU (>= 2 devices): plan devices on distinct GPUs, transfers peer-to-peer over NVLink."""
+import pytest
+
+from common import MIXED_SPECS, O_TOL, LSE_TOL, bundle_for, inputs, lse_err, rel_err
+
+pytestmark = pytest.mark.gpu
+
+
+def _ngpu():
+    import torch
+    return torch.cuda.device_count()
+
+
+@pytest.mark.parametrize("R", [2, 4])
+def test_multi_gpu_forward_backward(R):
+    if _ngpu() < 2:
+        pytest.skip("needs >= 2 GPUs")
+    import torch
+
+    import oracle as O
+    from paper_2510_10620_b200.executor import DCPExecutor
+    bundle = bundle_for(MIXED_SPECS, H=4, G=2, block=256, R=R)
+    (q, k, v), (q64, k64, v64) = inputs(bundle, seed=7)
+    g = torch.Generator().manual_seed(9)
+    d_o = torch.randn((bundle.total_tokens, 4, 128), generator=g).to(torch.bfloat16)
+    devs = [d % _ngpu() for d in range(R)]
+    ex = DCPExecutor(devs)
+    ex.prepare(bundle)
+    T = bundle.total_tokens
+    o = torch.zeros((T, 4, 128), dtype=torch.bfloat16, device="cuda:0")
+    lse = torch.zeros((4, T), device="cuda:0")
+    dq = torch.zeros_like(o)
+    dk = torch.zeros((T, 2, 128), dtype=torch.bfloat16, device="cuda:0")
+    dv = torch.zeros_like(dk)
+    ex.load_inputs(q.cuda(), k.cuda(), v.cuda())
+    rep = ex.forward(o, lse)
+    ex.backward(d_o.cuda(), dq, dk, dv)
+    ex.synchronize()
+    o_ref, lse_ref, orep, st, msg = O.run(bundle, q64, k64, v64)
+    assert rel_err(o.float().cpu().numpy(), o_ref) <= O_TOL
+    assert lse_err(lse.cpu().numpy(), lse_ref) <= LSE_TOL
+    assert rep["total_bytes"] == orep.total_bytes
+    rq, rk, rv = O.dense_backward(bundle, q64, k64, v64, d_o.double().numpy())
+    assert rel_err(dq.float().cpu().numpy(), rq) <= O_TOL
+    assert rel_err(dk.float().cpu().numpy(), rk) <= O_TOL
+    assert rel_err(dv.float().cpu().numpy(), rv) <= O_TOL
+    ex.close()
