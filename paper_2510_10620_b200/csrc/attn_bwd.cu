@@ -9,15 +9,15 @@
 // accumulating dK and dV in TMEM. dQ of each step is reduce-added (fp32) into the
 // q slot's dQ accumulator.
 //
-// CTA = 384 threads, persistent:
+// CTA = 512 threads, persistent:
 //   warp 0      TMA producer: K, V per unit; Q, dO tiles + LSE/Delta rows per step (2 stages)
 //   warp 1      TMEM owner + tcgen05.mma issuer
 //   warps 2-3   idle (register donors)
 //   warps 4-11  compute: warp group c = 0/1 handles q columns [64c, 64c+64) of every kv row
-//               (TMEM lane = kv row): P^T -> TMEM, dS^T -> smem (SW128); then drain the dQ
-//               columns [64c, 64c+64) of every q row: TMEM -> smem (fp32, SW128) -> TMA
-//               bulk-tensor reduce-add into the dQ accumulator; at the end of a unit
-//               group 0 adds dV and group 1 adds dK to the fp32 accumulators.
+//               (TMEM lane = kv row): P^T -> TMEM, dS^T -> smem (SW128); at the end of a
+//               unit group 0 adds dV and group 1 adds dK to the fp32 accumulators.
+//   warps 12-15 dQ drain: TMEM -> the step's Q/dO stage buffers (fp32, SW128) -> TMA
+//               bulk-tensor reduce-add into the dQ accumulator.
 // TMEM: S^T [0,128) (P^T bf16 overwrites [0,64)), dP^T [128,256) (reused for dQ),
 //       dV [256,384), dK [384,512).
 // Masks: for partial tiles each lane builds 32-bit words "q row -> kv rows of my warp"
@@ -31,7 +31,7 @@
 
 namespace dcpx {
 
-constexpr int kBwdThreads = 384;
+constexpr int kBwdThreads = 512;
 // K 32K | V 32K | Q[2] 64K | dO[2] 64K | dS 32K | LSE[2] 1K | Delta[2] 1K | barriers
 constexpr int kBwdSmemMain = 224 * 1024;
 constexpr int kBwdSmem = kBwdSmemMain + 2048 + 256;
@@ -95,12 +95,12 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     mbar_init(&bars.kv_empty, 1);
     for (int i = 0; i < 2; ++i) {
       mbar_init(&bars.q_full[i], 1);
-      mbar_init(&bars.q_empty[i], 1);
+      mbar_init(&bars.q_empty[i], 2);  // MMA commit (dV, dK done) + drain (dQ staged and read)
     }
     mbar_init(&bars.s_full, 1);
     mbar_init(&bars.p_ready, 256);
     mbar_init(&bars.dq_full, 1);
-    mbar_init(&bars.dq_empty, 256);
+    mbar_init(&bars.dq_empty, 128);
     mbar_init(&bars.ds_free, 1);
     mbar_init(&bars.acc_full, 1);
     mbar_init(&bars.acc_empty, 256);
@@ -115,7 +115,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tbase = bars.tmem_base;
-  if (warp < 4) asm volatile("setmaxnreg.dec.sync.aligned.u32 88;");
+  if (warp < 4) asm volatile("setmaxnreg.dec.sync.aligned.u32 72;");
 
   if (warp == 0) {
     // ------------------------------------------------------------ producer
@@ -205,9 +205,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         umma_commit(&bars.kv_empty);
       }
     }
-  } else if (warp >= 4) {
+  } else if (warp >= 4 && warp < 12) {
     // ------------------------------------------------------------ compute warps
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 208;");
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 168;");
     const int c = (warp - 4) >> 2;                  // q-column half handled by this group
     const int wq = warp & 3;                        // TMEM lane quarter
     const int j = (wq << 5) + lane;                 // kv row (P/dS) / q row (dQ drain)
@@ -299,38 +299,6 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         fence_proxy_async_smem();
         tc_fence_before();
         mbar_arrive(&bars.p_ready);
-        // ---- dQ drain: q row j, columns [64c, 64c+64) of dQ (TMEM cols [128,256)).
-        // Staged as two [128 rows x 32 cols] fp32 chunks (128B-swizzled) through this
-        // group's own 16 KiB half of the dS buffer (free once dQ's MMA retired) and
-        // reduce-added into the dQ accumulator by one TMA bulk-tensor op per chunk.
-        mbar_wait(&bars.dq_full, g & 1);
-        tc_fence_after();
-        {
-          uint32_t v0[32], v1[32];
-          tmem_ld32(lane_addr + 128 + 64 * c, v0);
-          tmem_ld32(lane_addr + 128 + 64 * c + 32, v1);
-          tmem_wait_ld();
-          tc_fence_before();
-          mbar_arrive(&bars.dq_empty);
-          uint8_t* stage = sDS + c * 16384;
-#pragma unroll
-          for (int r = 0; r < 2; ++r) {
-            const uint32_t* v = r ? v1 : v0;
-            uint8_t* row = stage + j * 128;
-#pragma unroll
-            for (int q4 = 0; q4 < 8; ++q4)
-              *reinterpret_cast<uint4*>(row + ((q4 ^ (j & 7)) << 4)) =
-                  make_uint4(v[4 * q4], v[4 * q4 + 1], v[4 * q4 + 2], v[4 * q4 + 3]);
-            fence_proxy_async_smem();
-            named_bar_sync(2 + c, 128);
-            if (wq == 0 && lane == 0 && !(p.debug_flags & 1)) {
-              tma_reduce_add_2d(&tm_dq, stage, 64 * c + 32 * r, S.q_row0);
-              bulk_commit();
-              bulk_wait_read<0>();
-            }
-            named_bar_sync(2 + c, 128);
-          }
-        }
       }
       // ---- unit epilogue: group 0 adds dV [256,384), group 1 adds dK [384,512)
       mbar_wait(&bars.acc_full, it & 1);
@@ -350,6 +318,50 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       tc_fence_before();
       mbar_arrive(&bars.acc_empty);
     }
+  } else if (warp >= 12) {
+    // ------------------------------------------------------------ dQ drain warpgroup
+    // q row r of each step: dQ (TMEM cols [128,256)) -> four [128 x 32] fp32 chunks,
+    // 128B-swizzled, staged in the step's own Q / dO stage buffers (free once dV and dK
+    // retired: dq_full is committed after them) -> TMA bulk-tensor reduce-add into the
+    // dQ accumulator; the stage is handed back to the producer after TMA has read it.
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 104;");
+    const int wq = warp & 3;
+    const int r = (wq << 5) + lane;
+    const uint32_t lane_addr = tbase + ((uint32_t)(wq * 32) << 16);
+    uint32_t g = 0;
+    for (int u = blockIdx.x; u < p.num_units; u += gridDim.x) {
+      const BwdUnit U = p.units[u];
+      for (int s = 0; s < U.step_count; ++s, ++g) {
+        const int q_row0 = p.steps[U.step_begin + s].q_row0;
+        const int st = g & 1;
+        mbar_wait(&bars.dq_full, g & 1);
+        tc_fence_after();
+#pragma unroll 1
+        for (int k = 0; k < 4; ++k) {
+          uint32_t v[32];
+          tmem_ld32(lane_addr + 128 + 32 * k, v);
+          tmem_wait_ld();
+          uint8_t* chunk = (k < 2 ? sQ : sDO) + st * 32768 + (k & 1) * 16384 + r * 128;
+#pragma unroll
+          for (int q4 = 0; q4 < 8; ++q4)
+            *reinterpret_cast<uint4*>(chunk + ((q4 ^ (r & 7)) << 4)) =
+                make_uint4(v[4 * q4], v[4 * q4 + 1], v[4 * q4 + 2], v[4 * q4 + 3]);
+        }
+        tc_fence_before();
+        mbar_arrive(&bars.dq_empty);
+        fence_proxy_async_smem();
+        named_bar_sync(2, 128);
+        if (wq == 0 && lane == 0) {
+          if (!(p.debug_flags & 1))
+            for (int k = 0; k < 4; ++k)
+              tma_reduce_add_2d(&tm_dq, (k < 2 ? sQ : sDO) + st * 32768 + (k & 1) * 16384, 32 * k, q_row0);
+          bulk_commit();
+          bulk_wait_read<0>();
+          mbar_arrive(&bars.q_empty[st]);
+        }
+      }
+    }
+    if (wq == 0 && lane == 0) bulk_wait<0>();
   }
   tc_fence_before();
   __syncthreads();
