@@ -207,9 +207,13 @@ dcpx_status dcpx_synchronize(dcpx_ctx* ctx);
 /* Test / introspection hooks (not part of the reference surface). */
 /* Device pointers of the slot arenas of plan device `dev`: kind 0 Q, 1 KV, 2 O, 3 LSE. */
 dcpx_status dcpx_debug_arena(dcpx_ctx* ctx, int dev, int kind, void** ptr, int64_t* slot_rows);
-/* Executor options: key "fuse_reductions", "remap_copies", "check_rows", "timing". */
+/* Executor options: "fuse_reductions", "remap_copies", "timing", "kernel_timing", "trace". */
 dcpx_status dcpx_set_option(dcpx_ctx* ctx, const char* key, int64_t value);
 
+/* Op trace of the last forward/backward (option "trace"): rows of 7 doubles
+ * (plan device, instruction, op kind, division, pass 0 fwd / 1 bwd, start ms, end ms),
+ * times relative to the call's start on that device. Returns the number of rows. */
+int dcpx_trace(dcpx_ctx* ctx, double* rows, int max_rows);
 const char* dcpx_last_error(dcpx_ctx* ctx);
 const char* dcpx_version(void);
 void dcpx_destroy(dcpx_ctx* ctx);

@@ -91,10 +91,18 @@ dcpx_status dcpx_set_option(dcpx_ctx* ctx, const char* key, int64_t value) {
     else if (k == "remap_copies") ex.opt.remap_copies = value != 0;
     else if (k == "check_rows") ex.opt.check_rows = value != 0;
     else if (k == "timing") ex.opt.timing = value != 0;
+    else if (k == "trace") ex.opt.trace = value != 0;
+    else if (k == "sm_transfers") ex.opt.sm_transfers = value != 0;
+    else if (k == "sm_reserve") ex.opt.sm_reserve = static_cast<int>(value);
     else if (k == "kernel_timing") ex.opt.kernel_timing = value != 0;
     else if (k == "bwd_debug") ex.opt.bwd_debug = static_cast<int>(value);
     else throw dcpx::Failure(DCPX_ERROR, "unknown option " + k);
   });
+}
+
+int dcpx_trace(dcpx_ctx* ctx, double* rows, int max_rows) {
+  if (!ctx || !ctx->ex) return -1;
+  return ctx->ex->trace_rows(rows, max_rows);
 }
 
 const char* dcpx_last_error(dcpx_ctx* ctx) {

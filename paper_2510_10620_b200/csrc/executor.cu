@@ -128,7 +128,9 @@ Executor::Executor(int ndev, const int* ordinals) : R_(ndev) {
     DeviceGuard g(ordinals_[d]);
     dev_[d].ordinal = ordinals_[d];
     CUDA_OK(cudaStreamCreateWithFlags(&dev_[d].cs, cudaStreamNonBlocking));
-    CUDA_OK(cudaStreamCreateWithFlags(&dev_[d].ms, cudaStreamNonBlocking));
+    int lo = 0, hi = 0;
+    CUDA_OK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    CUDA_OK(cudaStreamCreateWithPriority(&dev_[d].ms, cudaStreamNonBlocking, hi));  // transfers first
     CUDA_OK(cudaEventCreate(&dev_[d].t0));
     CUDA_OK(cudaEventCreate(&dev_[d].t1));
   }
@@ -212,6 +214,67 @@ cudaEvent_t Executor::event(int d) {
     D.events.push_back(e);
   }
   return D.events[D.next_event++];
+}
+
+// Persistent attention grids leave `sm_reserve` SMs free when the plan communicates, so
+// transfer kernels on the (high-priority) comm stream run concurrently with compute.
+int Executor::attn_grid(int d, int grid) const {
+  const int reserve = opt.sm_reserve >= 0 ? opt.sm_reserve : (R_ > 1 ? 8 : 0);
+  const int cap = std::max(1, num_sms(dev_[d].ordinal) - reserve);
+  return std::min(grid, cap);
+}
+
+// LOCAL transport on the DMA copy engines: one peer copy per contiguous block component,
+// issued on the receiver's comm stream so NVLink traffic never competes with the
+// persistent attention kernels for SMs.
+void Executor::copy_engine(const std::vector<RowCopyJob>& jobs, cudaStream_t s) {
+  for (const auto& j : jobs) {
+    if (j.src_stride == j.row_bytes && j.dst_stride == j.row_bytes) {
+      CUDA_OK(cudaMemcpyAsync(j.dst, j.src, static_cast<size_t>(j.rows) * j.row_bytes, cudaMemcpyDefault, s));
+    } else {
+      CUDA_OK(cudaMemcpy2DAsync(j.dst, j.dst_stride, j.src, j.src_stride, j.row_bytes, j.rows, cudaMemcpyDefault, s));
+    }
+  }
+}
+
+// ---- op tracing (option "trace"): device-time spans of every executed op ------------------
+void Executor::trace_begin() {
+  trace_.clear();
+  trace_pending_.clear();
+}
+
+TraceScope::TraceScope(Executor* ex, int d, int instr, cudaStream_t s, int pass, const Op& op)
+    : ex_(ex), d_(d) {
+  if (!ex->opt.trace || op.kind == OpKind::kNop || op.kind == OpKind::kCommLaunch) return;
+  auto ev = ex->kernel_events(d);
+  CUDA_OK(cudaEventRecord(ev.first, s));
+  ex->trace_pending_.push_back({d, instr, static_cast<int>(op.kind), op.division, pass, ev.first, ev.second});
+  s_ = s;
+  active_ = true;
+}
+
+TraceScope::~TraceScope() {
+  if (active_) cudaEventRecord(ex_->trace_pending_.back().end, s_);
+}
+
+void Executor::trace_collect() {
+  for (const auto& t : trace_pending_) {
+    DeviceGuard gd(dev_[t.d].ordinal);
+    cudaEventSynchronize(t.end);
+    float a = 0, b = 0;
+    cudaEventElapsedTime(&a, dev_[t.d].t0, t.start);
+    cudaEventElapsedTime(&b, dev_[t.d].t0, t.end);
+    trace_.push_back({static_cast<double>(t.d), static_cast<double>(t.instr), static_cast<double>(t.kind),
+                      static_cast<double>(t.division), static_cast<double>(t.pass), a, b});
+  }
+  trace_pending_.clear();
+}
+
+int Executor::trace_rows(double* out, int max_rows) const {
+  const int n = std::min<int>(max_rows, static_cast<int>(trace_.size()));
+  for (int i = 0; i < n; ++i)
+    for (int k = 0; k < 7; ++k) out[7 * i + k] = trace_[i][k];
+  return static_cast<int>(trace_.size());
 }
 
 std::pair<cudaEvent_t, cudaEvent_t> Executor::kernel_events(int d) {
@@ -452,6 +515,7 @@ void Executor::prepare(int nplans, const dcpx_plan_view* plans, const dcpx_graph
         }
       }
       op.jobs = make_jobs(d, jobs);
+      op.xfer = jobs;
       op.peer = src_dev;
     }
     build_io_jobs(d);
@@ -900,10 +964,8 @@ void Executor::compile_device(int d) {
         J.n_rows = static_cast<int32_t>(SR);
         J.src_begin = 0;
         J.n_src = I.count;
-        std::vector<int32_t> srows;
-        for (int k = 0; k < I.count; ++k) srows.push_back(static_cast<int32_t>(D.o_phys[P.srcs[I.offset + k]] * SR));
-        op.src_rows = upload(d, srows);
-        op.jobs = make_row_jobs(d, std::vector<MergeJob>{J}, std::vector<int>{J.n_rows}, 16);
+        for (int k = 0; k < I.count; ++k) op.msrc.push_back(static_cast<int32_t>(D.o_phys[P.srcs[I.offset + k]] * SR));
+        op.mjobs.push_back(J);
         break;
       }
       case DCPX_OP_COPY: {
@@ -928,6 +990,18 @@ void Executor::compile_device(int d) {
         op.tag = I.tag;
         op.blocks.assign(P.blocks.begin() + I.offset, P.blocks.begin() + I.offset + I.count);
         for (const auto& tb : op.blocks) op.bytes += g_.data_blocks[tb.block].size_bytes;
+        if (I.send) {
+          // Q / KV sends read resident slots, written only by dcpx_load_inputs
+          std::set<int> res_q, res_kv;
+          for (const auto& r : P.res_q) res_q.insert(r.slot);
+          for (const auto& r : P.res_kv) res_kv.insert(r.slot);
+          op.resident_only = true;
+          for (const auto& tb : op.blocks) {
+            const int kd = g_.data_blocks[tb.block].kind;
+            if (!((kd == DCPX_KIND_Q && res_q.count(tb.slot)) || (kd == DCPX_KIND_KV && res_kv.count(tb.slot))))
+              op.resident_only = false;
+          }
+        }
         if (I.send) {  // snapshot semantics: the sent slots must not be rewritten afterwards
           for (const auto& tb : op.blocks)
             if (g_.data_blocks[tb.block].kind == DCPX_KIND_O && o_touched(P, g_, i + 1, tb.slot)) {
@@ -947,6 +1021,35 @@ void Executor::compile_device(int d) {
         op.tag = I.tag;
         break;
     }
+  }
+  // ---- 5. batch runs of independent consecutive reductions into one merge launch
+  for (size_t i = 0; i < D.prog.size(); ++i) {
+    if (D.prog[i].kind != OpKind::kMerge) continue;
+    Op& head = D.prog[i];
+    std::set<int32_t> touched;  // O-arena rows written or read by the run
+    for (const auto& J : head.mjobs) touched.insert(J.dst_row0);
+    for (int32_t r : head.msrc) touched.insert(r);
+    size_t k = i + 1;
+    for (; k < D.prog.size(); ++k) {
+      Op& o2 = D.prog[k];
+      if (o2.kind == OpKind::kNop) continue;
+      if (o2.kind != OpKind::kMerge) break;
+      bool clash = touched.count(o2.mjobs[0].dst_row0) > 0;
+      for (int32_t r : o2.msrc) clash |= touched.count(r) > 0 && r != o2.mjobs[0].dst_row0;
+      if (clash) break;
+      MergeJob J = o2.mjobs[0];
+      J.src_begin = static_cast<int32_t>(head.msrc.size());
+      head.mjobs.push_back(J);
+      head.msrc.insert(head.msrc.end(), o2.msrc.begin(), o2.msrc.end());
+      touched.insert(J.dst_row0);
+      touched.insert(o2.msrc.begin(), o2.msrc.end());
+      o2.kind = OpKind::kNop;
+    }
+    std::vector<int> rows;
+    for (const auto& J : head.mjobs) rows.push_back(J.n_rows);
+    head.src_rows = upload(d, head.msrc);
+    head.jobs = make_row_jobs(d, head.mjobs, rows, 16);
+    i = k - 1;
   }
   // final output slots (after copy remaps)
   D.final_o_slot.clear();
@@ -1044,6 +1147,7 @@ void Executor::build_bwd_jobs() {
         }
       }
       op.bjobs = make_jobs(d, jobs);
+      op.bxfer = jobs;
     }
     // 2. gradient returns of fetched blocks, right after the attention of their last use
     std::map<int, int> cur_q, cur_kv;                    // slot -> fetched block
@@ -1172,10 +1276,18 @@ void Executor::forward(void* o_out, float* lse_out, dcpx_report* rep, bool host)
     if (opt.timing) CUDA_OK(cudaEventRecord(D.t0, D.cs));
   }
   std::map<std::string, cudaEvent_t> send_ev, recv_ev;
+  std::vector<cudaEvent_t> ready_ev(static_cast<size_t>(R_));
+  for (int d = 0; d < R_; ++d) {  // resident Q / KV were scattered on cs before this call
+    DeviceGuard gd(dev_[d].ordinal);
+    ready_ev[d] = event(d);
+    CUDA_OK(cudaEventRecord(ready_ev[d], dev_[d].cs));
+  }
+  trace_begin();
   for (const auto& [d, i] : order_) {
     DevState& D = dev_[d];
     Op& op = D.prog[i];
     DeviceGuard gd(D.ordinal);
+    TraceScope ts(this, d, static_cast<int>(i), op.kind == OpKind::kCommWait ? D.ms : D.cs, 0, op);
     switch (op.kind) {
       case OpKind::kFwdAttn: {
         if (!op.num_units) break;
@@ -1186,7 +1298,7 @@ void Executor::forward(void* o_out, float* lse_out, dcpx_report* rep, bool host)
         p.scale_log2 = static_cast<float>(1.4426950408889634 / std::sqrt(static_cast<double>(g_.D)));
         std::pair<cudaEvent_t, cudaEvent_t> ke{};
         if (opt.kernel_timing) { ke = kernel_events(d); CUDA_OK(cudaEventRecord(ke.first, D.cs)); }
-        launch_attn_fwd(D.tm_q, D.tm_kv, p, op.grid, D.cs);
+        launch_attn_fwd(D.tm_q, D.tm_kv, p, attn_grid(d, op.grid), D.cs);
         if (opt.kernel_timing) CUDA_OK(cudaEventRecord(ke.second, D.cs));
         ++D.launches;
         break;
@@ -1200,16 +1312,24 @@ void Executor::forward(void* o_out, float* lse_out, dcpx_report* rep, bool host)
         ++D.launches;
         break;
       case OpKind::kCommLaunch: {
-        cudaEvent_t e = event(d);
-        CUDA_OK(cudaEventRecord(e, D.cs));
-        (op.send ? send_ev : recv_ev)[op.tag] = e;
+        if (op.send && op.resident_only) {
+          send_ev[op.tag] = ready_ev[d];  // resident inputs: ready since load / preprocess
+        } else {
+          cudaEvent_t e = event(d);
+          CUDA_OK(cudaEventRecord(e, D.cs));
+          (op.send ? send_ev : recv_ev)[op.tag] = e;
+        }
         break;
       }
       case OpKind::kCommWait: {
         CUDA_OK(cudaStreamWaitEvent(D.ms, send_ev.at(op.tag), 0));
         CUDA_OK(cudaStreamWaitEvent(D.ms, recv_ev.at(op.tag), 0));
-        launch_row_copy(op.jobs.dj, D.ms);
-        ++D.launches;
+        if (opt.sm_transfers) {
+          launch_row_copy(op.jobs.dj, D.ms);
+          ++D.launches;
+        } else {
+          copy_engine(op.xfer, D.ms);
+        }
         cudaEvent_t e = event(d);
         CUDA_OK(cudaEventRecord(e, D.ms));
         CUDA_OK(cudaStreamWaitEvent(D.cs, e, 0));
@@ -1255,6 +1375,7 @@ void Executor::forward(void* o_out, float* lse_out, dcpx_report* rep, bool host)
 }
 
 void Executor::fill_report(dcpx_report* rep, bool bwd) {
+  if (opt.trace) trace_collect();
   if (!rep) return;
   std::memset(rep, 0, sizeof(*rep));
   rep->devices = R_;
@@ -1383,11 +1504,19 @@ void Executor::backward(const void* d_o, void* dq, void* dk, void* dv, dcpx_repo
         }
   }
   std::map<std::string, cudaEvent_t> send_ev, recv_ev;
+  std::vector<cudaEvent_t> ready_ev(static_cast<size_t>(R_));
+  for (int d = 0; d < R_; ++d) {  // dO scattered, Delta / LSE prepared on cs
+    DeviceGuard gd(dev_[d].ordinal);
+    ready_ev[d] = event(d);
+    CUDA_OK(cudaEventRecord(ready_ev[d], dev_[d].cs));
+  }
+  trace_begin();
   for (const auto& [d, i] : order_) {
     DevState& D = dev_[d];
     Op& op = D.prog[i];
     if (plans_[d].ins[i].division >= T) continue;  // output stage has no backward counterpart
     DeviceGuard gd(D.ordinal);
+    TraceScope ts(this, d, static_cast<int>(i), op.kind == OpKind::kCommWait ? D.ms : D.cs, 1, op);
     switch (op.kind) {
       case OpKind::kFwdAttn: {
         if (op.bnum_units) {
@@ -1401,7 +1530,7 @@ void Executor::backward(const void* d_o, void* dq, void* dk, void* dv, dcpx_repo
           p.debug_flags = opt.bwd_debug;
           std::pair<cudaEvent_t, cudaEvent_t> ke{};
           if (opt.kernel_timing) { ke = kernel_events(d); CUDA_OK(cudaEventRecord(ke.first, D.cs)); }
-          launch_attn_bwd(D.tm_q, D.tm_do, D.tm_kv, D.tm_dq, p, op.bgrid, D.cs);
+          launch_attn_bwd(D.tm_q, D.tm_do, D.tm_kv, D.tm_dq, p, attn_grid(d, op.bgrid), D.cs);
           if (opt.kernel_timing) CUDA_OK(cudaEventRecord(ke.second, D.cs));
           ++D.launches;
         }
@@ -1412,16 +1541,24 @@ void Executor::backward(const void* d_o, void* dq, void* dk, void* dv, dcpx_repo
         break;
       }
       case OpKind::kCommLaunch: {
-        cudaEvent_t e = event(d);
-        CUDA_OK(cudaEventRecord(e, D.cs));
-        (op.send ? send_ev : recv_ev)[op.tag] = e;
+        if (op.send && op.resident_only) {
+          send_ev[op.tag] = ready_ev[d];  // resident inputs: ready since load / preprocess
+        } else {
+          cudaEvent_t e = event(d);
+          CUDA_OK(cudaEventRecord(e, D.cs));
+          (op.send ? send_ev : recv_ev)[op.tag] = e;
+        }
         break;
       }
       case OpKind::kCommWait: {
         CUDA_OK(cudaStreamWaitEvent(D.ms, send_ev.at(op.tag), 0));
         CUDA_OK(cudaStreamWaitEvent(D.ms, recv_ev.at(op.tag), 0));
-        launch_row_copy(op.bjobs.dj, D.ms);
-        ++D.launches;
+        if (opt.sm_transfers) {
+          launch_row_copy(op.bjobs.dj, D.ms);
+          ++D.launches;
+        } else {
+          copy_engine(op.bxfer, D.ms);
+        }
         cudaEvent_t e = event(d);
         CUDA_OK(cudaEventRecord(e, D.ms));
         CUDA_OK(cudaStreamWaitEvent(D.cs, e, 0));

@@ -4,6 +4,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <array>
 #include <map>
 #include <memory>
 #include <stdexcept>
@@ -77,8 +78,12 @@ struct Op {
   int bnum_units = 0, bgrid = 0;
   JobList ret;   // LOCAL: dQ / dK,dV partials of fetched blocks whose last use is here
   JobList bjobs; // kCommWait: backward payload transfer (Q + dO + LSE + Delta, or K + V)
+  std::vector<RowCopyJob> xfer, bxfer;  // the same transfers for the copy engines
+  std::vector<MergeJob> mjobs;          // kMerge (host side, batched before upload)
+  std::vector<int32_t> msrc;
   // comm
   int send = 0, peer = 0;
+  bool resident_only = false;  // a send of resident Q / KV slots only
   std::string tag;
   std::vector<dcpx_block_slot> blocks;
   uint64_t bytes = 0;
@@ -117,6 +122,24 @@ struct Options {
   bool timing = true;
   int bwd_debug = 0;
   bool kernel_timing = false;
+  bool trace = false;
+  bool sm_transfers = true;   // LOCAL transfers by copy kernel (false: DMA copy engines)
+  int sm_reserve = -1;        // SMs left free of attention CTAs for transfer kernels (-1: auto)
+};
+
+class Executor;
+
+// Records device-time spans of one executed op when Options::trace is set.
+class TraceScope {
+ public:
+  TraceScope(Executor* ex, int d, int instr, cudaStream_t s, int pass, const Op& op);
+  ~TraceScope();
+
+ private:
+  Executor* ex_;
+  int d_;
+  cudaStream_t s_ = nullptr;
+  bool active_ = false;
 };
 
 class Executor {
@@ -130,10 +153,22 @@ class Executor {
   void backward(const void* d_o, void* dq, void* dk, void* dv, dcpx_report* rep, bool host);
   void synchronize();
   void debug_arena(int dev, int kind, void** ptr, int64_t* rows);
+  int trace_rows(double* out, int max_rows) const;  // rows of 7: dev, instr, kind, division, pass, start_ms, end_ms
   Options opt;
   std::string last_error;
 
  private:
+  friend class TraceScope;
+  struct TracePending {
+    int d, instr, kind, division, pass;
+    cudaEvent_t start, end;
+  };
+  std::vector<TracePending> trace_pending_;
+  std::vector<std::array<double, 7>> trace_;
+  void trace_begin();
+  void copy_engine(const std::vector<RowCopyJob>& jobs, cudaStream_t s);
+  int attn_grid(int d, int grid) const;
+  void trace_collect();
   void compile_device(int d);
   void compile_attention(int d, int ins_index, std::vector<bool>& fused_red);
   void build_io_jobs(int d);

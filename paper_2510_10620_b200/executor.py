@@ -30,7 +30,7 @@ STATUS = {0: "OK", 1: "Error", 2: "DeadlockError", 3: "TagMismatchError", 4: "Bu
 EXPORTS = ["dcpx_create", "dcpx_create_rank", "dcpx_nccl_unique_id", "dcpx_prepare",
            "dcpx_load_inputs", "dcpx_load_inputs_host", "dcpx_forward", "dcpx_forward_host",
            "dcpx_backward", "dcpx_backward_host", "dcpx_synchronize", "dcpx_debug_arena",
-           "dcpx_set_option", "dcpx_last_error", "dcpx_version", "dcpx_destroy"]
+           "dcpx_set_option", "dcpx_trace", "dcpx_last_error", "dcpx_version", "dcpx_destroy"]
 
 
 class DCPXError(RuntimeError):
@@ -73,6 +73,8 @@ def lib():
         L.dcpx_last_error.argtypes = [C.c_void_p]
         L.dcpx_destroy.argtypes = [C.c_void_p]
         L.dcpx_nccl_unique_id.argtypes = [C.c_void_p]
+        L.dcpx_trace.argtypes = [C.c_void_p, C.c_void_p, C.c_int]
+        L.dcpx_trace.restype = C.c_int
         _lib = L
     return _lib
 
@@ -156,6 +158,16 @@ class DCPExecutor:
 
     def synchronize(self):
         self._check(lib().dcpx_synchronize(self._h))
+
+    def trace(self):
+        """Op spans of the last call when option "trace" is set: list of dicts."""
+        import numpy as np
+        n = lib().dcpx_trace(self._h, None, 0)
+        buf = np.zeros((max(n, 1), 7))
+        lib().dcpx_trace(self._h, buf.ctypes.data, n)
+        kinds = ["attn", "merge", "copy", "launch", "wait", "nop"]
+        return [dict(dev=int(r[0]), instr=int(r[1]), kind=kinds[int(r[2])], division=int(r[3]),
+                     pass_="bwd" if r[4] else "fwd", start=r[5], end=r[6]) for r in buf[:n]]
 
     def arena(self, dev: int, kind: int):
         ptr, rows = C.c_void_p(), C.c_int64()
