@@ -381,4 +381,8 @@ void launch_attn_bwd(const CUtensorMap& tm_q, const CUtensorMap& tm_do, const CU
   attn_bwd_kernel<<<grid, kBwdThreads, kBwdSmem, stream>>>(tm_q, tm_do, tm_kv, tm_dq, p);
 }
 
+void set_watchdog_buffer_bwd(uint32_t* diag) {
+  cudaMemcpyToSymbol(g_watchdog_diag, &diag, sizeof(diag));
+}
+
 }  // namespace dcpx

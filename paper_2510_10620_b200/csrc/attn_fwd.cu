@@ -376,4 +376,8 @@ void launch_attn_fwd(const CUtensorMap& tm_q, const CUtensorMap& tm_kv, const Fw
   attn_fwd_kernel<<<grid, kFwdThreads, kFwdSmem, stream>>>(tm_q, tm_kv, p);
 }
 
+void set_watchdog_buffer_fwd(uint32_t* diag) {
+  cudaMemcpyToSymbol(g_watchdog_diag, &diag, sizeof(diag));
+}
+
 }  // namespace dcpx

@@ -22,6 +22,7 @@ dcpx_status guarded(dcpx_ctx* ctx, F&& f) {
     return DCPX_OK;
   } catch (const dcpx::Failure& e) {
     ctx->err = e.what();
+    if (e.code == DCPX_CUDA_ERROR) ctx->err += ctx->ex->watchdog_info();
     return e.code;
   } catch (const std::exception& e) {
     ctx->err = e.what();

@@ -124,9 +124,14 @@ Executor::Executor(int ndev, const int* ordinals) : R_(ndev) {
           cudaGetLastError();
         }
       }
+  CUDA_OK(cudaHostAlloc(reinterpret_cast<void**>(&diag_), sizeof(uint32_t) * (1 + 4 * 64),
+                        cudaHostAllocMapped | cudaHostAllocPortable));
+  std::memset(diag_, 0, sizeof(uint32_t) * (1 + 4 * 64));
   for (int d = 0; d < R_; ++d) {
     DeviceGuard g(ordinals_[d]);
     dev_[d].ordinal = ordinals_[d];
+    set_watchdog_buffer_fwd(diag_);
+    set_watchdog_buffer_bwd(diag_);
     CUDA_OK(cudaStreamCreateWithFlags(&dev_[d].cs, cudaStreamNonBlocking));
     int lo = 0, hi = 0;
     CUDA_OK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
@@ -143,6 +148,7 @@ Executor::~Executor() {
     if (d.ms) cudaStreamSynchronize(d.ms);
   }
   free_all();
+  if (diag_) cudaFreeHost(diag_);
   for (auto& d : dev_) {
     DeviceGuard g(d.ordinal);
     for (auto e : d.events) cudaEventDestroy(e);
@@ -268,6 +274,18 @@ void Executor::trace_collect() {
                       static_cast<double>(t.division), static_cast<double>(t.pass), a, b});
   }
   trace_pending_.clear();
+}
+
+std::string Executor::watchdog_info() const {
+  if (!diag_ || diag_[0] == 0) return "";
+  std::string s = " [watchdog: " + std::to_string(diag_[0]) + " timed-out waits; distinct (block, warp, barrier, parity):";
+  std::set<std::tuple<uint32_t, uint32_t, uint32_t, uint32_t>> seen;
+  for (uint32_t i = 0; i < std::min<uint32_t>(diag_[0], 64); ++i)
+    seen.insert({diag_[1 + 4 * i], diag_[2 + 4 * i] / 32, diag_[3 + 4 * i], diag_[4 + 4 * i]});
+  for (const auto& [b, w, a, par] : seen)
+    s += " (" + std::to_string(b) + ", w" + std::to_string(w) + ", smem+" + std::to_string(a) + ", " +
+         std::to_string(par) + ")";
+  return s + "]";
 }
 
 int Executor::trace_rows(double* out, int max_rows) const {

@@ -153,7 +153,8 @@ class Executor {
   void backward(const void* d_o, void* dq, void* dk, void* dv, dcpx_report* rep, bool host);
   void synchronize();
   void debug_arena(int dev, int kind, void** ptr, int64_t* rows);
-  int trace_rows(double* out, int max_rows) const;  // rows of 7: dev, instr, kind, division, pass, start_ms, end_ms
+  int trace_rows(double* out, int max_rows) const;
+  std::string watchdog_info() const;  // barrier waits that timed out (kernel watchdog)  // rows of 7: dev, instr, kind, division, pass, start_ms, end_ms
   Options opt;
   std::string last_error;
 
@@ -188,6 +189,7 @@ class Executor {
   std::vector<std::pair<int, int>> order_;
   std::vector<void*> allocs_;  // (ordinal, ptr) freed in destructor
   std::vector<int> alloc_dev_;
+  uint32_t* diag_ = nullptr;   // host-mapped watchdog report buffer (see sm100.cuh)
   char* in_stage_ = nullptr;   // host-input staging on device 0 (load_inputs_host)
   char* out_stage_ = nullptr;  // host-output staging on device 0 (forward_host)
   char* bwd_stage_ = nullptr;  // host staging for backward (dO in, dQ/dK/dV out)

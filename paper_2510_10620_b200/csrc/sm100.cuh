@@ -77,21 +77,48 @@ __device__ __forceinline__ uint64_t global_ns() {
   return t;
 }
 
+// Hang diagnostics: when a wait times out, the waiting thread records (block, thread,
+// barrier shared-address, parity) into host-mapped memory (if the host registered a
+// buffer through the kernel parameters) before trapping, so a protocol bug can be located
+// after the launch fails. Layout: word 0 = record count, then 4 words per record.
+// Each translation unit gets its own copy (static); the host sets it per device through
+// set_watchdog_buffer_* (attn_fwd.cu / attn_bwd.cu). Only read on the timeout path.
+static __device__ uint32_t* g_watchdog_diag = nullptr;
+
+__device__ __forceinline__ void watchdog_report(uint32_t* diag, uint32_t addr, uint32_t parity) {
+  // producer / MMA warps (0-1) of every block, other roles of block 0 only
+  if (diag && (threadIdx.x & 31) == 0 && (threadIdx.x < 64 || blockIdx.x == 0)) {
+    const uint32_t i = atomicAdd(diag, 1u);
+    if (i < 64) {
+      diag[1 + 4 * i] = blockIdx.x;
+      diag[2 + 4 * i] = threadIdx.x;
+      diag[3 + 4 * i] = addr;
+      diag[4 + 4 * i] = parity;
+    }
+    __threadfence_system();
+  }
+}
+
 // Blocks until the phase with the given parity has completed. A watchdog traps after
-// ~20 s of waiting so a protocol bug surfaces as a launch error instead of a hung GPU.
+// ~10 s of waiting so a protocol bug surfaces as a launch error instead of a hung GPU.
+// Debug builds (-DDCPX_WATCHDOG_REPORT) also record the stuck barrier (watchdog_report)
+// before trapping; that path costs registers, so it is off in production builds.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   const uint32_t addr = smem_u32(bar);
-#ifndef DCPX_NO_WATCHDOG
   if (mbar_try_wait(addr, parity)) return;
   const uint64_t t0 = global_ns();
   uint32_t spins = 0;
   while (!mbar_try_wait(addr, parity)) {
-    if ((++spins & 1023u) == 0 && global_ns() - t0 > 20000000000ull) __trap();
-  }
-#else
-  while (!mbar_try_wait(addr, parity)) {
-  }
+    if ((++spins & 1023u) == 0 && global_ns() - t0 > 10000000000ull) {
+#ifdef DCPX_WATCHDOG_REPORT
+      watchdog_report(g_watchdog_diag, addr, parity);
+      const uint64_t t1 = global_ns();  // let the other stuck roles report before trapping
+      while (global_ns() - t1 < 2000000000ull) {
+      }
 #endif
+      __trap();
+    }
+  }
 }
 
 // ---- TMA -----------------------------------------------------------------------------

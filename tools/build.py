@@ -46,8 +46,9 @@ def build_dcpx(force=False):
     for s in srcs:
         o = os.path.join(objdir, os.path.basename(s) + ".o")
         if force or _stale(o, [s] + [d for d in deps if not d.endswith(".cu")]):
+            extra = ["-DDCPX_WATCHDOG_REPORT"] if os.environ.get("DCPX_DEBUG") else []
             _run([NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
-                  "-Xptxas", "-warn-spills", "-c", s, "-o", o])
+                  "-Xptxas", "-warn-spills", *extra, "-c", s, "-o", o])
         objs.append(o)
     _run([NVCC, *ARCH, "-shared", "-o", out, *objs, "-lcudart"])
     return out
