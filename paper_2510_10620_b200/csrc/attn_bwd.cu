@@ -4,27 +4,32 @@
 //   P = exp(s - LSE), dV = P^T dO, dP = dO V^T, Delta = rowsum(dO o O),
 //   dS = P o (dP - Delta), dQ = scale * dS K, dK = scale * dS^T Q.
 //
-// Work unit = one 128-row kv sub-tile of one KV slot; it streams every (item, 128-row
-// q tile) step of the division that touches it (all heads of the GQA group, all q tiles),
-// accumulating dK and dV in TMEM. dQ of each step is reduce-added (fp32) into the
-// q slot's dQ accumulator.
+// Work unit = one 128-row kv sub-tile of one KV slot; it streams (item, 64-row q tile)
+// steps of the division that touch it (all heads of the GQA group), accumulating dK and
+// dV in TMEM. dQ of each step is reduce-added (fp32, TMA) into the q slot's accumulator.
+//
+// Software pipeline: the MMA issuer runs S^T(g), dP^T(g) one step ahead of the gradient
+// MMAs dV(g-1), dK(g-1), dQ^T(g-1), and two compute warpgroups take alternate steps, so
+// the softmax-gradient math of step g overlaps the tensor work of step g-1.
 //
 // CTA = 512 threads, persistent:
-//   warp 0      TMA producer: K, V per unit; Q, dO tiles + LSE/Delta rows per step (2 stages)
+//   warp 0      TMA producer: K, V per unit; Q, dO tiles + LSE/Delta rows per step (4 stages)
 //   warp 1      TMEM owner + tcgen05.mma issuer
 //   warps 2-3   idle (register donors)
-//   warps 4-11  compute: warp group c = 0/1 handles q columns [64c, 64c+64) of every kv row
-//               (TMEM lane = kv row): P^T -> TMEM, dS^T -> smem (SW128); at the end of a
-//               unit group 0 adds dV and group 1 adds dK to the fp32 accumulators.
-//   warps 12-15 dQ drain: TMEM -> the step's Q/dO stage buffers (fp32, SW128) -> TMA
-//               bulk-tensor reduce-add into the dQ accumulator.
-// TMEM: S^T [0,128) (P^T bf16 overwrites [0,64)), dP^T [128,256) (reused for dQ),
-//       dV [256,384), dK [384,512).
+//   warps 4-7   compute group 0 (even steps), warps 8-11 compute group 1 (odd steps):
+//               TMEM lane = kv row; P^T (bf16) -> TMEM, dS^T -> smem (SW128). At the end
+//               of a unit group 0 adds dV and group 1 adds dK to the fp32 accumulators.
+//   warps 12-15 dQ drain: dQ^T (TMEM lane = head dim) -> the step's Q/dO stage buffers
+//               (fp32 [q][d], SW128) -> TMA bulk-tensor reduce-add into the accumulator.
+// TMEM (512 cols): slot b in {0,1} = S^T [128b, 128b+64) (P^T bf16 overwrites its first
+//       32 cols) | dP^T [128b+64, 128b+128) (reused for dQ^T); dV [256,384); dK [384,512).
 // Masks: for partial tiles each lane builds 32-bit words "q row -> kv rows of my warp"
 // from the q rows' <= 2 attend ranges and transposes them across the warp (5 shuffles),
 // giving every kv-row thread a bitmask over its q columns; the element loop is branch-free.
 #include <cuda_bf16.h>
 #include <math_constants.h>
+
+#include <cstdio>
 
 #include "program.h"
 #include "sm100.cuh"
@@ -32,14 +37,18 @@
 namespace dcpx {
 
 constexpr int kBwdThreads = 512;
-// K 32K | V 32K | Q[2] 64K | dO[2] 64K | dS 32K | LSE[2] 1K | Delta[2] 1K | barriers
-constexpr int kBwdSmemMain = 224 * 1024;
+constexpr int kBwdStages = 4;
+// K 32K | V 32K | dS^T[2] 32K | stages[4] x (Q 16K | dO 16K) | LSE[4] 1K | Delta[4] 1K | barriers
+constexpr int kBwdStageBytes = 32768;
+constexpr int kBwdSmemMain = (96 + 32 * kBwdStages) * 1024;
 constexpr int kBwdSmem = kBwdSmemMain + 2048 + 256;
+static_assert(kBwdSmem <= 232448, "backward shared memory exceeds the sm_100 opt-in limit");
 
 struct BwdBarriers {
   uint64_t kv_full, kv_empty;
-  uint64_t q_full[2], q_empty[2];
-  uint64_t s_full, p_ready, dq_full, dq_empty, ds_free, acc_full, acc_empty;
+  uint64_t q_full[kBwdStages], q_empty[kBwdStages];
+  uint64_t s_full[2], p_ready[2], dq_full[2], dq_empty[2], ds_free[2];
+  uint64_t acc_full, acc_empty;
   uint32_t tmem_base;
 };
 
@@ -72,18 +81,41 @@ __device__ __forceinline__ uint32_t warp_transpose32(uint32_t x, int lane) {
   return x;
 }
 
+// Wait-cycle accounting for pipeline tuning (-DDCPX_BWD_PROFILE builds only): CTA 0's
+// role leaders add the cycles spent in each wait and print them at exit.
+#ifdef DCPX_BWD_PROFILE
+#define BWD_PROF_DECL long long prof_[6] = {0, 0, 0, 0, 0, 0}; const long long prof_t0_ = clock64();
+#define BWD_TIMED(i, stmt)                  \
+  do {                                      \
+    const long long t_ = clock64();         \
+    stmt;                                   \
+    prof_[i] += clock64() - t_;             \
+  } while (0)
+#define BWD_PROF_PRINT(name, a, b, c, d, e, f)                                                            \
+  do {                                                                                                     \
+    if (blockIdx.x == 0)                                                                                   \
+      printf("[bwd prof] %-8s total %lld  %s %lld  %s %lld  %s %lld  %s %lld  %s %lld  %s %lld\n", name, \
+             clock64() - prof_t0_, a, prof_[0], b, prof_[1], c, prof_[2], d, prof_[3], e, prof_[4], f, prof_[5]); \
+  } while (0)
+#else
+#define BWD_PROF_DECL
+#define BWD_TIMED(i, stmt) stmt
+#define BWD_PROF_PRINT(name, a, b, c, d, e, f) \
+  do {                                         \
+  } while (0)
+#endif
+
 __global__ void __launch_bounds__(kBwdThreads, 1)
     attn_bwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_do,
                     const __grid_constant__ CUtensorMap tm_kv, const __grid_constant__ CUtensorMap tm_dq,
                     const BwdParams p) {
   extern __shared__ __align__(1024) uint8_t smem[];
-  uint8_t* sK = smem;
+  uint8_t* sK = smem;                 // [128 kv][128 d] as two SW128 halves of 64 d
   uint8_t* sV = smem + 32768;
-  uint8_t* sQ = smem + 65536;     // [2 stages][32 KiB]
-  uint8_t* sDO = smem + 131072;   // [2 stages][32 KiB]
-  uint8_t* sDS = smem + 196608;   // dS^T [kv rows][q], two q halves of 16 KiB, SW128
-  float* sLSE = reinterpret_cast<float*>(smem + kBwdSmemMain);          // [2][128] (log2 units)
-  float* sDelta = reinterpret_cast<float*>(smem + kBwdSmemMain + 1024);  // [2][128]
+  uint8_t* sDS = smem + 65536;        // [2][128 kv][64 q] bf16, SW128 rows of 128 B
+  uint8_t* sStage = smem + 98304;     // [4] x (Q [64 q][128 d] | dO [64 q][128 d]), halves of 64 d
+  float* sLSE = reinterpret_cast<float*>(smem + kBwdSmemMain);          // [4][64] (log2 units)
+  float* sDelta = reinterpret_cast<float*>(smem + kBwdSmemMain + 1024);  // [4][64]
   BwdBarriers& bars = *reinterpret_cast<BwdBarriers*>(smem + kBwdSmemMain + 2048);
 
   const int warp = threadIdx.x >> 5;
@@ -93,15 +125,17 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   if (threadIdx.x == 0) {
     mbar_init(&bars.kv_full, 1);
     mbar_init(&bars.kv_empty, 1);
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < kBwdStages; ++i) {
       mbar_init(&bars.q_full[i], 1);
-      mbar_init(&bars.q_empty[i], 2);  // MMA commit (dV, dK done) + drain (dQ staged and read)
+      mbar_init(&bars.q_empty[i], 1);  // drain: dQ staged in the stage and read by TMA
     }
-    mbar_init(&bars.s_full, 1);
-    mbar_init(&bars.p_ready, 256);
-    mbar_init(&bars.dq_full, 1);
-    mbar_init(&bars.dq_empty, 128);
-    mbar_init(&bars.ds_free, 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&bars.s_full[b], 1);
+      mbar_init(&bars.p_ready[b], 128);
+      mbar_init(&bars.dq_full[b], 1);
+      mbar_init(&bars.dq_empty[b], 128);
+      mbar_init(&bars.ds_free[b], 1);
+    }
     mbar_init(&bars.acc_full, 1);
     mbar_init(&bars.acc_empty, 256);
     fence_barrier_init();
@@ -119,121 +153,162 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 
   if (warp == 0) {
     // ------------------------------------------------------------ producer
-    if (lane == 0) {
+    // converged warp, one elected lane issues (keeps the TMA operands in uniform registers)
+    {
+      BWD_PROF_DECL
       uint32_t g = 0, it = 0;
       for (int u = blockIdx.x; u < p.num_units; u += gridDim.x, ++it) {
         const BwdUnit U = p.units[u];
-        mbar_wait(&bars.kv_empty, (it & 1) ^ 1);
-        mbar_arrive_expect_tx(&bars.kv_full, 65536);
-        for (int h = 0; h < 2; ++h) {
-          tma_load_2d(&tm_kv, &bars.kv_full, sK + h * 16384, 64 * h, U.kv_row0);
-          tma_load_2d(&tm_kv, &bars.kv_full, sV + h * 16384, 64 * h, U.kv_row0 + p.slot_rows);
+        BWD_TIMED(0, mbar_wait(&bars.kv_empty, (it & 1) ^ 1));
+        if (elect_one()) {
+          mbar_arrive_expect_tx(&bars.kv_full, 65536);
+          for (int h = 0; h < 2; ++h) {
+            tma_load_2d(&tm_kv, &bars.kv_full, sK + h * 16384, 64 * h, U.kv_row0);
+            tma_load_2d(&tm_kv, &bars.kv_full, sV + h * 16384, 64 * h, U.kv_row0 + p.slot_rows);
+          }
         }
+        __syncwarp();
         for (int j = 0; j < U.step_count; ++j, ++g) {
           const BwdStep S = p.steps[U.step_begin + j];
-          const int st = g & 1;
-          mbar_wait(&bars.q_empty[st], ((g >> 1) & 1) ^ 1);
-          mbar_arrive_expect_tx(&bars.q_full[st], 65536 + 1024);
-          for (int h = 0; h < 2; ++h) {
-            tma_load_2d(&tm_q, &bars.q_full[st], sQ + st * 32768 + h * 16384, 64 * h, S.q_row0);
-            tma_load_2d(&tm_do, &bars.q_full[st], sDO + st * 32768 + h * 16384, 64 * h, S.q_row0);
+          const int st = g % kBwdStages;
+          uint8_t* stage = sStage + st * kBwdStageBytes;
+          BWD_TIMED(1, mbar_wait(&bars.q_empty[st], ((g / kBwdStages) & 1) ^ 1));
+          if (elect_one()) {
+            mbar_arrive_expect_tx(&bars.q_full[st], kBwdStageBytes + 512);
+            for (int h = 0; h < 2; ++h) {
+              tma_load_2d(&tm_q, &bars.q_full[st], stage + h * 8192, 64 * h, S.q_row0);
+              tma_load_2d(&tm_do, &bars.q_full[st], stage + 16384 + h * 8192, 64 * h, S.q_row0);
+            }
+            bulk_load(sLSE + st * 64, p.lse2 + S.q_row0, 256, &bars.q_full[st]);
+            bulk_load(sDelta + st * 64, p.delta + S.q_row0, 256, &bars.q_full[st]);
           }
-          bulk_load(sLSE + st * 128, p.lse2 + S.q_row0, 512, &bars.q_full[st]);
-          bulk_load(sDelta + st * 128, p.delta + S.q_row0, 512, &bars.q_full[st]);
+          __syncwarp();
         }
       }
+      if (lane == 0) BWD_PROF_PRINT("producer", "kv_empty", "q_empty", "-", "-", "-", "-");
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
-    if (lane == 0) {
-      const uint32_t id_kmaj = idesc_bf16_f32(128, 128, 0, 0);   // A K-major, B K-major
-      const uint32_t id_bmn = idesc_bf16_f32(128, 128, 0, 1);    // A K-major, B MN-major
-      const uint32_t id_abmn = idesc_bf16_f32(128, 128, 1, 1);   // A MN-major, B MN-major
-      const uint32_t sk = smem_u32(sK), sv = smem_u32(sV), sq = smem_u32(sQ), sdo = smem_u32(sDO),
-                     sds = smem_u32(sDS);
+    // The whole warp runs the issue loop (converged, so descriptors stay in uniform
+    // registers) and one elected lane issues each batch of tcgen05 instructions; a
+    // lane-0-only loop makes ptxas wrap every MMA in an R2UR waterfall loop.
+    {
+      constexpr uint32_t id_s = idesc_bf16_f32(128, 64, 0, 0);   // S^T, dP^T: K-major A and B, N = 64 q
+      constexpr uint32_t id_g = idesc_bf16_f32(128, 128, 0, 1);  // dV, dK: B = Q / dO MN-major, N = 128 d
+      constexpr uint32_t id_q = idesc_bf16_f32(128, 64, 1, 1);   // dQ^T: A = K^T, B = dS^T, both MN-major
+      const uint32_t sk = smem_u32(sK), sv = smem_u32(sV), sds0 = smem_u32(sDS), sst = smem_u32(sStage);
+      BWD_PROF_DECL
+      // gradient MMAs of step g (stage st, slot b); first = first step of its unit
+      auto grads = [&](uint32_t g, bool first, uint32_t it) {
+        const uint32_t b = g & 1, st = g % kBwdStages;
+        const uint32_t sq = sst + st * kBwdStageBytes, sdo = sq + 16384, sds = sds0 + b * 16384;
+        BWD_TIMED(2, mbar_wait(&bars.p_ready[b], (g >> 1) & 1));
+        tc_fence_after();
+        if (first) {
+          BWD_TIMED(3, mbar_wait(&bars.acc_empty, (it & 1) ^ 1));
+          tc_fence_after();
+        }
+        if (elect_one()) {
+          // dV += P^T dO   (A = P^T in TMEM, K = 64 q; B = dO MN-major)
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk)
+            umma_ts(tbase + 256, tbase + 128 * b + kk * 8, sdesc_sw128(sdo + kk * 2048, 8192, 1024), id_g,
+                    (!first || kk > 0) ? 1u : 0u);
+          // dK += dS^T Q   (A = dS^T K-major; B = Q MN-major)
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk)
+            umma_ss(tbase + 384, sdesc_sw128(sds + kk * 32, 16, 1024), sdesc_sw128(sq + kk * 2048, 8192, 1024),
+                    id_g, (!first || kk > 0) ? 1u : 0u);
+          // dQ^T = K^T dS^T (A = K MN-major over d, B = dS^T MN-major over q; K = 128 kv) -> dP^T slot
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk)
+            umma_ss(tbase + 128 * b + 64, sdesc_sw128(sk + kk * 2048, 16384, 1024),
+                    sdesc_sw128(sds + kk * 2048, 8192, 1024), id_q, kk > 0);
+          umma_commit(&bars.dq_full[b]);
+          umma_commit(&bars.ds_free[b]);
+        }
+        __syncwarp();
+      };
       uint32_t g = 0, it = 0;
       for (int u = blockIdx.x; u < p.num_units; u += gridDim.x, ++it) {
         const BwdUnit U = p.units[u];
-        mbar_wait(&bars.kv_full, it & 1);
+        BWD_TIMED(4, mbar_wait(&bars.kv_full, it & 1));
         tc_fence_after();
         for (int j = 0; j < U.step_count; ++j, ++g) {
-          const int st = g & 1;
-          mbar_wait(&bars.q_full[st], (g >> 1) & 1);
+          const uint32_t b = g & 1, st = g % kBwdStages;
+          const uint32_t sq = sst + st * kBwdStageBytes, sdo = sq + 16384;
+          BWD_TIMED(0, mbar_wait(&bars.q_full[st], (g / kBwdStages) & 1));
           tc_fence_after();
-          // S^T = K Q^T  -> cols [0,128)
-          for (int kk = 0; kk < 8; ++kk) {
-            const uint32_t off = (kk >> 2) * 16384 + (kk & 3) * 32;
-            umma_ss(tbase, sdesc_sw128(sk + off, 16, 1024), sdesc_sw128(sq + st * 32768 + off, 16, 1024),
-                    id_kmaj, kk > 0);
+          // S^T = K Q^T -> slot b cols [0,64). Its previous occupant P^T(g-2) was read by
+          // dV(g-2), issued earlier on this thread.
+          if (elect_one()) {
+#pragma unroll
+            for (int kk = 0; kk < 8; ++kk)
+              umma_ss(tbase + 128 * b, sdesc_sw128(sk + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024),
+                      sdesc_sw128(sq + (kk >> 2) * 8192 + (kk & 3) * 32, 16, 1024), id_s, kk > 0);
           }
-          // dP^T = V dO^T -> cols [128,256) once the previous dQ has been drained
-          if (g > 0) {
-            mbar_wait(&bars.dq_empty, (g - 1) & 1);
+          __syncwarp();
+          // dP^T = V dO^T -> slot b cols [64,128), once dQ^T(g-2) has been drained from there
+          if (g >= 2) {
+            BWD_TIMED(1, mbar_wait(&bars.dq_empty[b], ((g >> 1) - 1) & 1));
             tc_fence_after();
           }
-          for (int kk = 0; kk < 8; ++kk) {
-            const uint32_t off = (kk >> 2) * 16384 + (kk & 3) * 32;
-            umma_ss(tbase + 128, sdesc_sw128(sv + off, 16, 1024), sdesc_sw128(sdo + st * 32768 + off, 16, 1024),
-                    id_kmaj, kk > 0);
+          if (elect_one()) {
+#pragma unroll
+            for (int kk = 0; kk < 8; ++kk)
+              umma_ss(tbase + 128 * b + 64, sdesc_sw128(sv + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024),
+                      sdesc_sw128(sdo + (kk >> 2) * 8192 + (kk & 3) * 32, 16, 1024), id_s, kk > 0);
+            umma_commit(&bars.s_full[b]);
           }
-          umma_commit(&bars.s_full);
-          mbar_wait(&bars.p_ready, g & 1);
-          tc_fence_after();
-          if (j == 0) {
-            mbar_wait(&bars.acc_empty, (it & 1) ^ 1);
-            tc_fence_after();
-          }
-          // dV += P^T dO   (A = P^T in TMEM, B = dO MN-major)
-          for (int kk = 0; kk < 8; ++kk)
-            umma_ts(tbase + 256, tbase + kk * 8, sdesc_sw128(sdo + st * 32768 + kk * 2048, 16384, 1024), id_bmn,
-                    (j > 0 || kk > 0) ? 1u : 0u);
-          // dK += dS^T Q   (A = dS^T K-major in smem, B = Q MN-major)
-          for (int kk = 0; kk < 8; ++kk) {
-            const uint32_t off = (kk >> 2) * 16384 + (kk & 3) * 32;
-            umma_ss(tbase + 384, sdesc_sw128(sds + off, 16, 1024),
-                    sdesc_sw128(sq + st * 32768 + kk * 2048, 16384, 1024), id_bmn, (j > 0 || kk > 0) ? 1u : 0u);
-          }
-          umma_commit(&bars.q_empty[st]);
-          // dQ = dS K      (A = dS MN-major in smem, B = K MN-major) -> cols [128,256)
-          for (int kk = 0; kk < 8; ++kk)
-            umma_ss(tbase + 128, sdesc_sw128(sds + kk * 2048, 16384, 1024), sdesc_sw128(sk + kk * 2048, 16384, 1024),
-                    id_abmn, kk > 0);
-          umma_commit(&bars.dq_full);
-          umma_commit(&bars.ds_free);
+          __syncwarp();
+          if (j > 0) grads(g - 1, j == 1, it);
         }
-        umma_commit(&bars.acc_full);
-        umma_commit(&bars.kv_empty);
+        grads(g - 1, U.step_count == 1, it);
+        if (elect_one()) {
+          umma_commit(&bars.acc_full);
+          umma_commit(&bars.kv_empty);
+        }
+        __syncwarp();
       }
+      if (lane == 0) BWD_PROF_PRINT("mma", "q_full", "dq_empty", "p_ready", "acc_empty", "kv_full", "-");
     }
   } else if (warp >= 4 && warp < 12) {
-    // ------------------------------------------------------------ compute warps
+    // ------------------------------------------------------------ compute warpgroups
     asm volatile("setmaxnreg.inc.sync.aligned.u32 168;");
-    const int c = (warp - 4) >> 2;                  // q-column half handled by this group
+    const uint32_t grp = (warp - 4) >> 2;           // steps with (g & 1) == grp
     const int wq = warp & 3;                        // TMEM lane quarter
-    const int j = (wq << 5) + lane;                 // kv row (P/dS) / q row (dQ drain)
+    const int j = (wq << 5) + lane;                 // kv row
     const uint32_t lane_addr = tbase + ((uint32_t)(wq * 32) << 16);
+    uint8_t* my_row0 = sDS + j * 128;
+    BWD_PROF_DECL
     uint32_t g = 0, it = 0;
     for (int u = blockIdx.x; u < p.num_units; u += gridDim.x, ++it) {
       const BwdUnit U = p.units[u];
       const bool kv_valid = j < U.n_kv;
-      // step descriptors are loaded one step ahead so their latency hides behind the work
-      BwdStep s_next = p.steps[U.step_begin];
-      ItemMask m_next = p.items[s_next.item];
-      for (int s = 0; s < U.step_count; ++s, ++g) {
+      // descriptors of my next step are loaded a step ahead so their latency hides
+      int s = (int)((grp - g) & 1);
+      BwdStep s_next{};
+      ItemMask m_next{};
+      if (s < U.step_count) {
+        s_next = p.steps[U.step_begin + s];
+        m_next = p.items[s_next.item];
+      }
+      for (; s < U.step_count; s += 2) {
+        const uint32_t gs = g + s;
         const BwdStep S = s_next;
         const ItemMask im = m_next;
-        if (s + 1 < U.step_count) {
-          s_next = p.steps[U.step_begin + s + 1];
+        if (s + 2 < U.step_count) {
+          s_next = p.steps[U.step_begin + s + 2];
           m_next = p.items[s_next.item];
         }
-        const int st = g & 1;
-        // ---- mask bits over my 64 q columns: mb[h] bit i <-> q column 64c + 32h + i
+        const uint32_t b = grp, st = gs % kBwdStages;
+        // ---- mask bits over the 64 q columns: mb[h] bit i <-> q column 32h + i
         uint32_t mb[2];
         if (S.cls == kTilePartial) {
           const int64_t base = im.kv_shift + S.col0 + 32 * wq;  // range coords of my warp's kv row 0
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
-            const int qi = 64 * c + 32 * h + lane;           // q row this lane describes
+            const int qi = 32 * h + lane;  // q row this lane describes
             uint32_t w = 0u;
             if (qi < S.n_q) {
               const int4 rg = __ldg(reinterpret_cast<const int4*>(p.ranges) + im.range_row0 + S.q_local0 + qi);
@@ -243,27 +318,25 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           }
         } else {
 #pragma unroll
-          for (int h = 0; h < 2; ++h) mb[h] = bits_in(0, S.n_q - 64 * c - 32 * h);
+          for (int h = 0; h < 2; ++h) mb[h] = bits_in(0, S.n_q - 32 * h);
         }
         if (!kv_valid) mb[0] = mb[1] = 0u;
-        mbar_wait(&bars.s_full, g & 1);
+        BWD_TIMED(0, mbar_wait(&bars.s_full[b], (gs >> 1) & 1));
         tc_fence_after();
-        if (g > 0) mbar_wait(&bars.ds_free, (g - 1) & 1);
-        const float4* lse4 = reinterpret_cast<const float4*>(sLSE + st * 128 + 64 * c);
-        const float4* dlt4 = reinterpret_cast<const float4*>(sDelta + st * 128 + 64 * c);
-        // P^T (bf16) lands in S^T columns [0,64): every S^T column must be read by both
-        // groups before either group stores P.
+        if (gs >= 2) BWD_TIMED(1, mbar_wait(&bars.ds_free[b], ((gs >> 1) - 1) & 1));
+        const float4* lse4 = reinterpret_cast<const float4*>(sLSE + st * 64);
+        const float4* dlt4 = reinterpret_cast<const float4*>(sDelta + st * 64);
+        const uint32_t slot = lane_addr + 128 * b;
         uint32_t srr[2][32];
-        tmem_ld32(lane_addr + 64 * c, srr[0]);
-        tmem_ld32(lane_addr + 64 * c + 32, srr[1]);
+        tmem_ld32(slot, srr[0]);
+        tmem_ld32(slot + 32, srr[1]);
         tmem_wait_ld();
-        named_bar_sync(1, 256);
+        uint8_t* row = my_row0 + b * 16384;
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
-          const int col = 64 * c + 32 * h;  // first q column of this chunk
           const uint32_t* sr = srr[h];
           uint32_t dr[32];
-          tmem_ld32(lane_addr + 128 + col, dr);
+          tmem_ld32(slot + 64 + 32 * h, dr);
           tmem_wait_ld();
           uint32_t pk[16], dk[16];
 #pragma unroll
@@ -285,9 +358,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
             dk[2 * e4] = pack_bf16(sv[0], sv[1]);
             dk[2 * e4 + 1] = pack_bf16(sv[2], sv[3]);
           }
-          tmem_st16(lane_addr + (col >> 1), pk);
-          // dS^T row j, q columns [col, col+32): 4 chunks of 16 B in half c, 128B-swizzled
-          uint8_t* row = sDS + c * 16384 + j * 128;
+          // P^T row j, q columns [32h, 32h+32) as bf16 pairs -> slot cols [16h, 16h+16)
+          tmem_st16(slot + 16 * h, pk);
+          // dS^T row j, q columns [32h, 32h+32): 16-byte chunks 4h..4h+3, 128B-swizzled
 #pragma unroll
           for (int q4 = 0; q4 < 4; ++q4) {
             const int chunk = 4 * h + q4;
@@ -298,13 +371,14 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         tmem_wait_st();
         fence_proxy_async_smem();
         tc_fence_before();
-        mbar_arrive(&bars.p_ready);
+        mbar_arrive(&bars.p_ready[b]);
       }
+      g += U.step_count;
       // ---- unit epilogue: group 0 adds dV [256,384), group 1 adds dK [384,512)
-      mbar_wait(&bars.acc_full, it & 1);
+      BWD_TIMED(2, mbar_wait(&bars.acc_full, it & 1));
       tc_fence_after();
-      float* dst = p.dkv_acc + ((int64_t)U.kv_row0 + (c == 0 ? p.slot_rows : 0) + j) * 128;
-      const uint32_t col = c == 0 ? 256 : 384;
+      float* dst = p.dkv_acc + ((int64_t)U.kv_row0 + (grp == 0 ? p.slot_rows : 0) + j) * 128;
+      const uint32_t col = grp == 0 ? 256 : 384;
 #pragma unroll 1
       for (int cc = 0; cc < 128; cc += 32) {
         uint32_t r[32];
@@ -318,50 +392,52 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       tc_fence_before();
       mbar_arrive(&bars.acc_empty);
     }
+    if (lane == 0 && wq == 0) BWD_PROF_PRINT(grp ? "compute1" : "compute0", "s_full", "ds_free", "acc_full", "-", "-", "-");
   } else if (warp >= 12) {
     // ------------------------------------------------------------ dQ drain warpgroup
-    // q row r of each step: dQ (TMEM cols [128,256)) -> four [128 x 32] fp32 chunks,
-    // 128B-swizzled, staged in the step's own Q / dO stage buffers (free once dV and dK
-    // retired: dq_full is committed after them) -> TMA bulk-tensor reduce-add into the
-    // dQ accumulator; the stage is handed back to the producer after TMA has read it.
+    // dQ^T of step g sits in slot g&1 cols [64,128) with TMEM lane = head dim d. Thread d
+    // writes column d of four [64 q][32 d] fp32 chunks (128B-swizzled; chunk k = d / 32)
+    // into the step's own stage buffer (free: dq_full is committed after dV and dK), then
+    // one thread reduce-adds them into the dQ accumulator and hands the stage back.
     asm volatile("setmaxnreg.dec.sync.aligned.u32 104;");
     const int wq = warp & 3;
-    const int r = (wq << 5) + lane;
     const uint32_t lane_addr = tbase + ((uint32_t)(wq * 32) << 16);
+    const uint32_t gran = (uint32_t)(lane >> 2), sub = (uint32_t)(lane & 3) * 4;
+    BWD_PROF_DECL
     uint32_t g = 0;
     for (int u = blockIdx.x; u < p.num_units; u += gridDim.x) {
       const BwdUnit U = p.units[u];
       for (int s = 0; s < U.step_count; ++s, ++g) {
         const int q_row0 = p.steps[U.step_begin + s].q_row0;
-        const int st = g & 1;
-        mbar_wait(&bars.dq_full, g & 1);
+        const uint32_t b = g & 1, st = g % kBwdStages;
+        uint8_t* stage = sStage + st * kBwdStageBytes;
+        BWD_TIMED(0, mbar_wait(&bars.dq_full[b], (g >> 1) & 1));
         tc_fence_after();
-#pragma unroll 1
-        for (int k = 0; k < 4; ++k) {
-          uint32_t v[32];
-          tmem_ld32(lane_addr + 128 + 32 * k, v);
-          tmem_wait_ld();
-          uint8_t* chunk = (k < 2 ? sQ : sDO) + st * 32768 + (k & 1) * 16384 + r * 128;
-#pragma unroll
-          for (int q4 = 0; q4 < 8; ++q4)
-            *reinterpret_cast<uint4*>(chunk + ((q4 ^ (r & 7)) << 4)) =
-                make_uint4(v[4 * q4], v[4 * q4 + 1], v[4 * q4 + 2], v[4 * q4 + 3]);
-        }
+        uint32_t v[2][32];
+        tmem_ld32(lane_addr + 128 * b + 64, v[0]);
+        tmem_ld32(lane_addr + 128 * b + 96, v[1]);
+        tmem_wait_ld();
         tc_fence_before();
-        mbar_arrive(&bars.dq_empty);
+        mbar_arrive(&bars.dq_empty[b]);
+        uint8_t* chunk = stage + wq * 8192 + sub;
+#pragma unroll
+        for (int q = 0; q < 64; ++q)
+          *reinterpret_cast<uint32_t*>(chunk + q * 128 + ((gran ^ (q & 7)) << 4)) = v[q >> 5][q & 31];
         fence_proxy_async_smem();
-        named_bar_sync(2, 128);
+        BWD_TIMED(1, named_bar_sync(2, 128));
         if (wq == 0 && lane == 0) {
           if (!(p.debug_flags & 1))
-            for (int k = 0; k < 4; ++k)
-              tma_reduce_add_2d(&tm_dq, (k < 2 ? sQ : sDO) + st * 32768 + (k & 1) * 16384, 32 * k, q_row0);
+            for (int k = 0; k < 4; ++k) tma_reduce_add_2d(&tm_dq, stage + k * 8192, 32 * k, q_row0);
           bulk_commit();
-          bulk_wait_read<0>();
+          BWD_TIMED(2, bulk_wait_read<0>());
           mbar_arrive(&bars.q_empty[st]);
         }
       }
     }
-    if (wq == 0 && lane == 0) bulk_wait<0>();
+    if (wq == 0 && lane == 0) {
+      bulk_wait<0>();
+      BWD_PROF_PRINT("drain", "dq_full", "bar", "tma_read", "-", "-", "-");
+    }
   }
   tc_fence_before();
   __syncthreads();

@@ -90,43 +90,57 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   if (warp < 4) asm volatile("setmaxnreg.dec.sync.aligned.u32 88;");
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
-    if (lane == 0) {
+    // converged warp, one elected lane issues (keeps the TMA operands in uniform registers)
+    {
       uint32_t g = 0, it = 0;
       for (int u = blockIdx.x; u < p.num_units; u += gridDim.x, ++it) {
         const FwdUnit U = p.units[u];
         const int ntiles = U.n_rows > kTileRows ? 2 : 1;
         mbar_wait(&bars.q_empty, (it & 1) ^ 1);
-        mbar_arrive_expect_tx(&bars.q_full, ntiles * 32768);
-        for (int t = 0; t < ntiles; ++t)
-          for (int h = 0; h < 2; ++h)
-            tma_load_2d(&tm_q, &bars.q_full, sQ + (t * 2 + h) * 16384, 64 * h, U.q_row0 + 128 * t);
+        if (elect_one()) {
+          mbar_arrive_expect_tx(&bars.q_full, ntiles * 32768);
+          for (int t = 0; t < ntiles; ++t)
+            for (int h = 0; h < 2; ++h)
+              tma_load_2d(&tm_q, &bars.q_full, sQ + (t * 2 + h) * 16384, 64 * h, U.q_row0 + 128 * t);
+        }
+        __syncwarp();
         for (int j = 0; j < U.step_count; ++j, ++g) {
           const FwdStep S = p.steps[U.step_begin + j];
           const int st = g & 1;
           mbar_wait(&bars.kv_empty[st], ((g >> 1) & 1) ^ 1);
-          mbar_arrive_expect_tx(&bars.k_full[st], 32768);
-          tma_load_2d(&tm_kv, &bars.k_full[st], sK + (st * 2 + 0) * 16384, 0, S.kv_row0);
-          tma_load_2d(&tm_kv, &bars.k_full[st], sK + (st * 2 + 1) * 16384, 64, S.kv_row0);
-          mbar_arrive_expect_tx(&bars.v_full[st], 32768);
-          tma_load_2d(&tm_kv, &bars.v_full[st], sV + (st * 2 + 0) * 16384, 0, S.kv_row0 + p.slot_rows);
-          tma_load_2d(&tm_kv, &bars.v_full[st], sV + (st * 2 + 1) * 16384, 64, S.kv_row0 + p.slot_rows);
+          if (elect_one()) {
+            mbar_arrive_expect_tx(&bars.k_full[st], 32768);
+            tma_load_2d(&tm_kv, &bars.k_full[st], sK + (st * 2 + 0) * 16384, 0, S.kv_row0);
+            tma_load_2d(&tm_kv, &bars.k_full[st], sK + (st * 2 + 1) * 16384, 64, S.kv_row0);
+            mbar_arrive_expect_tx(&bars.v_full[st], 32768);
+            tma_load_2d(&tm_kv, &bars.v_full[st], sV + (st * 2 + 0) * 16384, 0, S.kv_row0 + p.slot_rows);
+            tma_load_2d(&tm_kv, &bars.v_full[st], sV + (st * 2 + 1) * 16384, 64, S.kv_row0 + p.slot_rows);
+          }
+          __syncwarp();
         }
       }
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
-    if (lane == 0) {
-      const uint32_t id_s = idesc_bf16_f32(128, 128, 0, 0);  // Q K^T : both K-major
-      const uint32_t id_o = idesc_bf16_f32(128, 128, 0, 1);  // P V   : V is MN-major
+    // The converged warp runs the loop and one elected lane issues each batch of
+    // tcgen05 instructions (a lane-0-only loop makes ptxas wrap every MMA in an R2UR
+    // waterfall loop, which caps the issue rate well below the tensor pipe's).
+    {
+      constexpr uint32_t id_s = idesc_bf16_f32(128, 128, 0, 0);  // Q K^T : both K-major
+      constexpr uint32_t id_o = idesc_bf16_f32(128, 128, 0, 1);  // P V   : V is MN-major
       const uint32_t sq = smem_u32(sQ), sk = smem_u32(sK), sv = smem_u32(sV);
       uint32_t g = 0, it = 0, cnt_p[2] = {0, 0}, cnt_o[2] = {0, 0};
       auto issue_s = [&](int t, int st) {
-        for (int kk = 0; kk < 8; ++kk) {
-          const uint32_t off = (kk >> 2) * 16384 + (kk & 3) * 32;
-          umma_ss(tbase + 128 * t, sdesc_sw128(sq + t * 32768 + off, 16, 1024),
-                  sdesc_sw128(sk + st * 32768 + off, 16, 1024), id_s, kk > 0);
+        if (elect_one()) {
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk) {
+            const uint32_t off = (kk >> 2) * 16384 + (kk & 3) * 32;
+            umma_ss(tbase + 128 * t, sdesc_sw128(sq + t * 32768 + off, 16, 1024),
+                    sdesc_sw128(sk + st * 32768 + off, 16, 1024), id_s, kk > 0);
+          }
+          umma_commit(&bars.s_full[t]);
         }
-        umma_commit(&bars.s_full[t]);
+        __syncwarp();
       };
       for (int u = blockIdx.x; u < p.num_units; u += gridDim.x, ++it) {
         const FwdUnit U = p.units[u];
@@ -165,10 +179,14 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
               mbar_wait(&bars.o_empty[t], (cnt_o[t] & 1) ^ 1);
               tc_fence_after();
             }
-            for (int kk = 0; kk < 8; ++kk)
-              umma_ts(tbase + 256 + 128 * t, tbase + 128 * t + kk * 8,
-                      sdesc_sw128(sv + st * 32768 + kk * 2048, 16384, 1024), id_o,
-                      (!first[t] || kk > 0) ? 1u : 0u);
+            if (elect_one()) {
+#pragma unroll
+              for (int kk = 0; kk < 8; ++kk)
+                umma_ts(tbase + 256 + 128 * t, tbase + 128 * t + kk * 8,
+                        sdesc_sw128(sv + st * 32768 + kk * 2048, 16384, 1024), id_o,
+                        (!first[t] || kk > 0) ? 1u : 0u);
+            }
+            __syncwarp();
             first[t] = false;
             if (j + 1 < U.step_count && cls_of(steps[j + 1].cls, t)) {
               const uint32_t g2 = g + 1;
@@ -178,15 +196,18 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
               issued[t] = j + 1;
             }
           }
-          umma_commit(&bars.kv_empty[st]);
+          if (elect_one()) umma_commit(&bars.kv_empty[st]);
+          __syncwarp();
         }
-        umma_commit(&bars.q_empty);
+        if (elect_one()) {
+          umma_commit(&bars.q_empty);
+          for (int t = 0; t < 2; ++t)
+            if (has[t]) umma_commit(&bars.o_full[t]);
+        }
+        __syncwarp();
 #pragma unroll
         for (int t = 0; t < 2; ++t)
-          if (has[t]) {
-            umma_commit(&bars.o_full[t]);
-            ++cnt_o[t];
-          }
+          if (has[t]) ++cnt_o[t];
       }
     }
   } else if (warp >= 4) {

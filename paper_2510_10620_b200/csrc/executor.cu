@@ -59,13 +59,13 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
-// 2-D bf16 tensor map over an arena of `rows` x 128, box 128 rows x 64 columns,
+// 2-D bf16 tensor map over an arena of `rows` x 128, box `box_rows` rows x 64 columns,
 // 128-byte swizzle (matches the UMMA SWIZZLE_128B descriptors in sm100.cuh).
-CUtensorMap make_tmap(void* base, int64_t rows) {
+CUtensorMap make_tmap(void* base, int64_t rows, uint32_t box_rows = 128) {
   CUtensorMap m;
   cuuint64_t dims[2] = {128, static_cast<cuuint64_t>(rows)};
   cuuint64_t strides[1] = {256};
-  cuuint32_t box[2] = {64, 128};
+  cuuint32_t box[2] = {64, box_rows};
   cuuint32_t es[2] = {1, 1};
   CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, base, dims, strides, box, es,
                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -74,13 +74,13 @@ CUtensorMap make_tmap(void* base, int64_t rows) {
   return m;
 }
 
-// 2-D fp32 tensor map over a [rows][128] accumulator, box 128 rows x 32 columns (128 B),
+// 2-D fp32 tensor map over a [rows][128] accumulator, box 64 rows x 32 columns (128 B),
 // 128-byte swizzle: the TMA reduce-add target of the backward's dQ drain.
 CUtensorMap make_tmap_f32(void* base, int64_t rows) {
   CUtensorMap m;
   cuuint64_t dims[2] = {128, static_cast<cuuint64_t>(rows)};
   cuuint64_t strides[1] = {512};
-  cuuint32_t box[2] = {32, 128};
+  cuuint32_t box[2] = {32, kBwdQRows};
   cuuint32_t es[2] = {1, 1};
   CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, base, dims, strides, box, es,
                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -795,9 +795,10 @@ void Executor::compile_device(int d) {
     CUDA_OK(cudaMemset(D.d_o, 0, nq * SR * 256));
     CUDA_OK(cudaMemset(D.lse2, 0, nq * SR * 4));
     CUDA_OK(cudaMemset(D.delta, 0, nq * SR * 4));
-    D.tm_do = make_tmap(D.d_o, nq * SR);
+    D.tm_do = make_tmap(D.d_o, nq * SR, kBwdQRows);
     D.tm_dq = make_tmap_f32(D.dq_acc, nq * SR);
     D.tm_q = make_tmap(D.q, std::max<int64_t>(1, D.cap_q) * SR);
+    D.tm_q64 = make_tmap(D.q, std::max<int64_t>(1, D.cap_q) * SR, kBwdQRows);
     D.tm_kv = make_tmap(D.kv, std::max<int64_t>(1, D.cap_kv) * 2 * SR);
     std::vector<int32_t> ranges = g_.ranges;
     ranges.insert(ranges.end(), P.rows.begin(), P.rows.end());
@@ -817,7 +818,7 @@ void Executor::compile_device(int d) {
         op.kind = OpKind::kFwdAttn;
         // -- classify every item once: [128-row q tile][128-col kv sub-tile] -> empty /
         //    partial / full, from the item rows (plan.hpp:231-242 or explicit rows)
-        struct ItemCls { int nks = 0, n_qt = 0, mask = 0; std::vector<uint8_t> cls; };
+        struct ItemCls { int nks = 0, n_qt = 0, n_qb = 0, mask = 0; std::vector<uint8_t> cls, cls_b; };
         std::map<int, ItemCls> icl;
         std::vector<ItemMask> masks;
         for (int k = 0; k < I.count; ++k) {
@@ -828,6 +829,7 @@ void Executor::compile_device(int d) {
           ItemCls c;
           c.nks = (n_k + 127) / 128;
           c.n_qt = (n_q + 127) / 128;
+          c.n_qb = (n_q + kBwdQRows - 1) / kBwdQRows;
           ItemMask im{};
           im.n_k = n_k;
           const int32_t* rg;
@@ -843,6 +845,8 @@ void Executor::compile_device(int d) {
           c.mask = static_cast<int>(masks.size());
           masks.push_back(im);
           std::vector<uint8_t> all_full(static_cast<size_t>(c.n_qt) * c.nks, 1), any(static_cast<size_t>(c.n_qt) * c.nks, 0);
+          // the backward's 64-row q tiles
+          std::vector<uint8_t> all_full_b(static_cast<size_t>(c.n_qb) * c.nks, 1), any_b(static_cast<size_t>(c.n_qb) * c.nks, 0);
           uint64_t pairs = 0;
           for (int r = 0; r < n_q; ++r) {
             RelRange rr;
@@ -863,12 +867,17 @@ void Executor::compile_device(int d) {
               const bool hit = (rr.e0 > rr.b0 && rr.b0 < c1 && rr.e0 > c0) || (rr.e1 > rr.b1 && rr.b1 < c1 && rr.e1 > c0);
               if (!full) all_full[qt * c.nks + ks] = 0;
               if (hit) any[qt * c.nks + ks] = 1;
+              if (!full) all_full_b[(r / kBwdQRows) * c.nks + ks] = 0;
+              if (hit) any_b[(r / kBwdQRows) * c.nks + ks] = 1;
             }
           }
           op.flops += 4ull * pairs * static_cast<uint64_t>(g_.D);
           c.cls.resize(static_cast<size_t>(c.n_qt) * c.nks);
           for (size_t q = 0; q < c.cls.size(); ++q)
             c.cls[q] = !any[q] ? kTileEmpty : (all_full[q] ? kTileFull : kTilePartial);
+          c.cls_b.resize(static_cast<size_t>(c.n_qb) * c.nks);
+          for (size_t q = 0; q < c.cls_b.size(); ++q)
+            c.cls_b[q] = !any_b[q] ? kTileEmpty : (all_full_b[q] ? kTileFull : kTilePartial);
           icl[idx] = std::move(c);
         }
         // -- forward units: one per (group, pair of 128-row q tiles)
@@ -921,13 +930,18 @@ void Executor::compile_device(int d) {
         op.items = upload(d, masks);
         op.num_units = static_cast<int>(sorted.size());
         op.grid = std::min(op.num_units, num_sms(D.ordinal));
-        // -- backward units: one per (kv slot, 128-row kv sub-tile), streaming every
-        //    (item, q tile) of this instruction that reads it
+        // -- backward units: one per (kv slot, 128-row kv sub-tile, window of bwd_window
+        //    q tiles of one item). Windowing bounds the rows a wave of CTAs touches: with
+        //    units ordered by q window, the CTAs running at once stream the same Q / dO
+        //    tiles and reduce into the same fp32 dQ rows, which then stay in L2 instead
+        //    of making an HBM round trip per step; dK / dV are flushed per unit.
         std::map<int, std::vector<int>> by_kv;
         for (int k = 0; k < I.count; ++k) by_kv[P.items[I.offset + k].kv_slot].push_back(static_cast<int>(I.offset) + k);
         std::vector<BwdUnit> bunits;
         std::vector<BwdStep> bsteps;
         std::vector<int64_t> bcost;
+        std::vector<std::pair<int64_t, int64_t>> bkey;
+        const int win = opt.bwd_window > 0 ? opt.bwd_window : (1 << 30);
         for (const auto& [kv_slot, idxs] : by_kv) {
           const auto& f = P.items[idxs[0]];
           const int n_k = static_cast<int>(f.kv_end - f.kv_begin);
@@ -937,33 +951,54 @@ void Executor::compile_device(int d) {
             U.kv_row0 = static_cast<int32_t>(2 * kv_slot * SR + 128 * ks);
             U.n_kv = std::min(128, n_k - 128 * ks);
             U.step_begin = static_cast<int32_t>(bsteps.size());
+            int64_t cur_window = -1;
+            auto close = [&]() {
+              U.step_count = static_cast<int32_t>(bsteps.size()) - U.step_begin;
+              if (U.step_count > 0) {
+                bunits.push_back(U);
+                bcost.push_back(U.step_count);
+                bkey.emplace_back(bsteps[U.step_begin].q_row0, U.kv_row0);
+              }
+              U.step_begin = static_cast<int32_t>(bsteps.size());
+            };
             for (int idx : idxs) {
               const auto& it = P.items[idx];
               if (it.kv_end - it.kv_begin != n_k) throw Failure(DCPX_ERROR, "kv slot read with two sizes in one instruction");
               const auto& c = icl.at(idx);
               const int n_q = static_cast<int>(it.q_end - it.q_begin);
-              for (int qt = 0; qt < c.n_qt; ++qt) {
-                const uint32_t cl = c.cls[qt * c.nks + ks];
+              for (int qt = 0; qt < c.n_qb; ++qt) {
+                const uint32_t cl = c.cls_b[qt * c.nks + ks];
                 if (!cl) continue;
+                const int64_t window = static_cast<int64_t>(idx) * (1 << 20) + qt / win;
+                if (window != cur_window) {
+                  close();
+                  cur_window = window;
+                }
                 BwdStep S{};
-                S.q_row0 = static_cast<int32_t>(it.q_slot * SR + 128 * qt);
-                S.n_q = std::min(128, n_q - 128 * qt);
+                S.q_row0 = static_cast<int32_t>(it.q_slot * SR + kBwdQRows * qt);
+                S.n_q = std::min(kBwdQRows, n_q - kBwdQRows * qt);
                 S.item = c.mask;
-                S.q_local0 = 128 * qt;
+                S.q_local0 = kBwdQRows * qt;
                 S.col0 = 128 * ks;
                 S.cls = cl;
                 bsteps.push_back(S);
               }
             }
-            U.step_count = static_cast<int32_t>(bsteps.size()) - U.step_begin;
-            if (U.step_count == 0) continue;
-            bunits.push_back(U);
-            bcost.push_back(U.step_count);
+            close();
           }
         }
         std::vector<size_t> border(bunits.size());
         std::iota(border.begin(), border.end(), 0);
-        std::stable_sort(border.begin(), border.end(), [&](size_t a, size_t b) { return bcost[a] > bcost[b]; });
+        // bwd_order 0: longest-first; 1: plan order (kv slot, sub-tile, q window);
+        // 2: q window major, so consecutive units (one wave) share their Q / dO / dQ rows
+        if (opt.bwd_order == 0)
+          std::stable_sort(border.begin(), border.end(), [&](size_t a, size_t b) { return bcost[a] > bcost[b]; });
+        else if (opt.bwd_order == 2)
+          std::stable_sort(border.begin(), border.end(), [&](size_t a, size_t b) {
+            const int64_t wa = bkey[a].first / (int64_t{kBwdQRows} * std::min(win, 1 << 20));
+            const int64_t wb = bkey[b].first / (int64_t{kBwdQRows} * std::min(win, 1 << 20));
+            return wa != wb ? wa < wb : bkey[a].second < bkey[b].second;
+          });
         std::vector<BwdUnit> bsorted;
         for (size_t k : border) bsorted.push_back(bunits[k]);
         op.bunits = upload(d, bsorted);
@@ -1548,7 +1583,7 @@ void Executor::backward(const void* d_o, void* dq, void* dk, void* dv, dcpx_repo
           p.debug_flags = opt.bwd_debug;
           std::pair<cudaEvent_t, cudaEvent_t> ke{};
           if (opt.kernel_timing) { ke = kernel_events(d); CUDA_OK(cudaEventRecord(ke.first, D.cs)); }
-          launch_attn_bwd(D.tm_q, D.tm_do, D.tm_kv, D.tm_dq, p, attn_grid(d, op.bgrid), D.cs);
+          launch_attn_bwd(D.tm_q64, D.tm_do, D.tm_kv, D.tm_dq, p, attn_grid(d, op.bgrid), D.cs);
           if (opt.kernel_timing) CUDA_OK(cudaEventRecord(ke.second, D.cs));
           ++D.launches;
         }

@@ -104,7 +104,7 @@ struct DevState {
   // backward arenas (parallel to Q / KV arenas) and their io jobs
   __nv_bfloat16* d_o = nullptr;
   float *lse2 = nullptr, *delta = nullptr, *dq_acc = nullptr, *dkv_acc = nullptr;
-  CUtensorMap tm_do{}, tm_dq{};
+  CUtensorMap tm_do{}, tm_dq{}, tm_q64{};  // backward: 64-row boxes over dO, dQ acc, Q
   JobList scatter_do, prep, gather_dq, gather_dk, gather_dv;
   std::vector<int32_t> final_o_slot;  // per resident_o entry: physical slot holding the result
   std::vector<cudaEvent_t> events;
@@ -125,6 +125,8 @@ struct Options {
   bool trace = false;
   bool sm_transfers = true;   // LOCAL transfers by copy kernel (false: DMA copy engines)
   int sm_reserve = -1;        // SMs left free of attention CTAs for transfer kernels (-1: auto)
+  int bwd_order = 0;          // backward unit order (0 longest-first, 1 plan order, 2 q window)
+  int bwd_window = 0;         // 64-row q tiles per backward unit (0: a unit streams them all)
 };
 
 class Executor;

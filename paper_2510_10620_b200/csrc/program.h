@@ -16,6 +16,7 @@ namespace dcpx {
 
 constexpr int kHeadDim = 128;
 constexpr int kTileRows = 128;
+constexpr int kBwdQRows = 64;  // q rows per backward step
 
 // Mask classification of one (q tile, kv sub-tile) pair, 2 bits per q tile.
 enum : uint32_t { kTileEmpty = 0, kTilePartial = 1, kTileFull = 2 };
@@ -65,8 +66,8 @@ struct CopySeg {
   int64_t bytes;  // multiple of 16
 };
 
-// One backward work unit: a 128-row kv sub-tile of one KV slot, streaming all q tiles
-// of all items of the division that read it.
+// One backward work unit: a 128-row kv sub-tile of one KV slot, streaming 64-row q tiles
+// of the items of the division that read it.
 struct BwdUnit {
   int32_t kv_row0;  // KV arena row of the K sub-tile (V and the dV accumulator at + slot_rows)
   int32_t n_kv;     // valid kv rows (1..128)
@@ -75,8 +76,8 @@ struct BwdUnit {
 };
 
 struct BwdStep {
-  int32_t q_row0;    // Q / dO / LSE / Delta / dQ-accumulator row of this 128-row q tile
-  int32_t n_q;       // valid q rows (1..128)
+  int32_t q_row0;    // Q / dO / LSE / Delta / dQ-accumulator row of this 64-row q tile
+  int32_t n_q;       // valid q rows (1..64)
   int32_t item;      // ItemMask index
   int32_t q_local0;  // q row index within the item of tile row 0
   int32_t col0;      // kv-tile-relative index of the unit's kv row 0

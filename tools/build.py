@@ -37,16 +37,22 @@ def build_dcpx(force=False):
     srcs = sorted(glob.glob(os.path.join(csrc, "*.cu")))
     deps = srcs + glob.glob(os.path.join(csrc, "*.h")) + glob.glob(os.path.join(csrc, "*.cuh")) + \
         [os.path.join(REPO, "include", "dcpx.h")]
-    out = os.path.join(REPO, "paper_2510_10620_b200", "libdcpx.so")
+    # instrumented variants build into build/<variant>/ (never over the product library)
+    variant = "debug" if os.environ.get("DCPX_DEBUG") else "prof" if os.environ.get("DCPX_PROFILE") else ""
+    out = os.path.join(REPO, "build", variant, "libdcpx.so") if variant else \
+        os.path.join(REPO, "paper_2510_10620_b200", "libdcpx.so")
     if not force and not _stale(out, deps):
         return out
-    objdir = os.path.join(REPO, "build", "obj")
+    os.makedirs(os.path.dirname(out), exist_ok=True)
+    objdir = os.path.join(REPO, "build", "obj" + (f"_{variant}" if variant else ""))
     os.makedirs(objdir, exist_ok=True)
     objs = []
     for s in srcs:
         o = os.path.join(objdir, os.path.basename(s) + ".o")
         if force or _stale(o, [s] + [d for d in deps if not d.endswith(".cu")]):
             extra = ["-DDCPX_WATCHDOG_REPORT"] if os.environ.get("DCPX_DEBUG") else []
+            if os.environ.get("DCPX_PROFILE"):  # per-role wait-cycle counters printed by CTA 0
+                extra.append("-DDCPX_BWD_PROFILE")
             _run([NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
                   "-Xptxas", "-warn-spills", *extra, "-c", s, "-o", o])
         objs.append(o)

@@ -23,9 +23,10 @@ def main():
     k = torch.randn((T, G, 128), device="cuda", generator=g).to(torch.bfloat16)
     v = torch.randn((T, G, 128), device="cuda", generator=g).to(torch.bfloat16)
     ex = DCPExecutor([0] * b.R)
+    for opt in sys.argv[3:]:
+        key, _, val = opt.partition("=")
+        ex.set_option(key, int(val))
     ex.prepare(b)
-    if len(sys.argv) > 3:
-        ex.set_option('bwd_debug', int(sys.argv[3]))
     o = torch.empty((T, H, 128), dtype=torch.bfloat16, device="cuda")
     lse = torch.empty((H, T), device="cuda")
     ex.load_inputs(q, k, v)

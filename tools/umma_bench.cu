@@ -1,0 +1,127 @@
+// umma_bench.cu — issue-rate microbenchmark for the tcgen05.mma shapes and operand
+// layouts the attention kernels use (bf16 in, fp32 accumulate, SW128 operands).
+// One CTA per SM; warp 0 issues `iters` MMAs back to back, commits, waits, and reports
+// cycles per MMA. WARP=false: lane 0 alone runs the issue loop (divergent region);
+// WARP=true: the converged warp runs it and one elected lane issues each MMA.
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I paper_2510_10620_b200/csrc \
+//        tools/umma_bench.cu -o build/umma_bench && build/umma_bench
+#include <cstdio>
+#include <cuda_runtime.h>
+
+#include "sm100.cuh"
+
+using namespace dcpx;
+
+template <int N, int AMN, int BMN, bool TS, int NACC, bool WARP>
+__global__ void __launch_bounds__(128, 1) bench(int iters, long long* out) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ uint64_t bar;
+  __shared__ uint32_t tbase_s;
+  for (int i = threadIdx.x; i < 96 * 1024 / 4; i += blockDim.x)
+    reinterpret_cast<uint32_t*>(smem)[i] = 0x3c003c00u ^ (i * 2654435761u & 0x00ff00ffu);
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    fence_barrier_init();
+  }
+  if (threadIdx.x < 32) tmem_alloc<512>(&tbase_s);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = tbase_s;
+  constexpr uint32_t a_lbo = AMN ? 16384 : 16, b_lbo = BMN ? 8192 : 16;
+  constexpr uint32_t a_ks = AMN ? 2048 : 32, b_ks = BMN ? 2048 : 32;
+  constexpr uint32_t id = idesc_bf16_f32(128, N, AMN, BMN);
+  const uint32_t sa = smem_u32(smem), sb = smem_u32(smem) + 32768;
+  auto issue = [&](int i) {
+    const int kk = i & 3;
+    const uint32_t d = tbase + (NACC > 1 ? (uint32_t)((i % NACC) * N) : 0u);
+    if constexpr (TS)
+      umma_ts(d, tbase + 256 + kk * 8, sdesc_sw128(sb + kk * b_ks, b_lbo, 1024), id, 1);
+    else
+      umma_ss(d, sdesc_sw128(sa + kk * a_ks, a_lbo, 1024), sdesc_sw128(sb + kk * b_ks, b_lbo, 1024), id, 1);
+  };
+  long long t0 = 0, t1 = 0;
+  if constexpr (WARP) {
+    if (threadIdx.x < 32) {
+      fence_proxy_async_smem();
+      t0 = clock64();
+      for (int i = 0; i < iters; i += 4) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          if (elect_one()) issue(i + k);
+        __syncwarp();
+      }
+      if (elect_one()) umma_commit(&bar);
+      __syncwarp();
+      mbar_wait(&bar, 0);
+      t1 = clock64();
+    }
+  } else {
+    if (threadIdx.x == 0) {
+      fence_proxy_async_smem();
+      t0 = clock64();
+      for (int i = 0; i < iters; i += 4) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) issue(i + k);
+      }
+      umma_commit(&bar);
+      mbar_wait(&bar, 0);
+      t1 = clock64();
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) out[0] = t1 - t0;
+  tc_fence_before();
+  __syncthreads();
+  if (threadIdx.x < 32) tmem_dealloc<512>(tbase);
+}
+
+template <int N, int AMN, int BMN, bool TS, int NACC, bool WARP>
+void run(const char* name, long long* d_out, int sms) {
+  auto k = bench<N, AMN, BMN, TS, NACC, WARP>;
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+  const int iters = 8192;
+  for (int rep = 0; rep < 2; ++rep) k<<<sms, 128, 96 * 1024>>>(iters, d_out);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  cudaEventRecord(e0);
+  k<<<sms, 128, 96 * 1024>>>(iters, d_out);
+  cudaEventRecord(e1);
+  cudaError_t err = cudaDeviceSynchronize();
+  if (err != cudaSuccess) {
+    printf("%s: %s\n", name, cudaGetErrorString(err));
+    return;
+  }
+  long long cyc = 0;
+  cudaMemcpy(&cyc, d_out, 8, cudaMemcpyDeviceToHost);
+  float ms = 0;
+  cudaEventElapsedTime(&ms, e0, e1);
+  const double flop = 2.0 * 128 * N * 16 * (double)iters * sms;
+  printf("%-5s acc=%d %-34s %7.1f cyc/MMA  %7.1f TFLOP/s\n", WARP ? "warp" : "lane", NACC, name, (double)cyc / iters,
+         flop / (ms * 1e-3) / 1e12);
+}
+
+template <bool W>
+void all(long long* d, int sms) {
+  run<128, 0, 0, false, 1, W>("SS K/K   N=128", d, sms);
+  run<64, 0, 0, false, 1, W>("SS K/K   N=64", d, sms);
+  run<256, 0, 0, false, 1, W>("SS K/K   N=256", d, sms);
+  run<128, 0, 1, false, 1, W>("SS K/MN  N=128", d, sms);
+  run<128, 0, 1, true, 1, W>("TS -/MN  N=128", d, sms);
+  run<128, 0, 0, true, 1, W>("TS -/K   N=128", d, sms);
+  run<64, 1, 1, false, 1, W>("SS MN/MN N=64", d, sms);
+  run<128, 1, 1, false, 1, W>("SS MN/MN N=128", d, sms);
+  run<64, 0, 0, false, 2, W>("SS K/K   N=64 (2 accumulators)", d, sms);
+  run<128, 0, 0, false, 2, W>("SS K/K   N=128 (2 accumulators)", d, sms);
+}
+
+int main() {
+  setvbuf(stdout, nullptr, _IONBF, 0);
+  long long* d_out;
+  cudaMalloc(&d_out, 8);
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  all<false>(d_out, sms);
+  all<true>(d_out, sms);
+  return 0;
+}
