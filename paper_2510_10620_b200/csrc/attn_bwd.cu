@@ -13,16 +13,18 @@
 // the softmax-gradient math of step g overlaps the tensor work of step g-1.
 //
 // CTA = 512 threads, persistent:
-//   warp 0      TMA producer: K, V per unit; Q, dO tiles + LSE/Delta rows per step (4 stages)
+//   warp 0      TMA producer: Q, dO tiles + LSE/Delta rows per step (3 stages)
 //   warp 1      TMEM owner + tcgen05.mma issuer
-//   warps 2-3   idle (register donors)
+//   warp 2      TMA producer: K, V per unit
+//   warp 3      idle (register donor)
 //   warps 4-7   compute group 0 (even steps), warps 8-11 compute group 1 (odd steps):
 //               TMEM lane = kv row; P^T (bf16) -> TMEM, dS^T -> smem (SW128). At the end
 //               of a unit group 0 adds dV and group 1 adds dK to the fp32 accumulators.
 //   warps 12-15 dQ drain: dQ^T (TMEM lane = head dim) -> the step's Q/dO stage buffers
 //               (fp32 [q][d], SW128) -> TMA bulk-tensor reduce-add into the accumulator.
-// TMEM (512 cols): slot b in {0,1} = S^T [128b, 128b+64) (P^T bf16 overwrites its first
-//       32 cols) | dP^T [128b+64, 128b+128) (reused for dQ^T); dV [256,384); dK [384,512).
+// TMEM (512 cols): slot b in {0,1} = S^T [128b, 128b+64) (then P^T and dS^T as bf16 in its
+//       two 32-col halves: A operands of dV and dK) | dP^T [128b+64, 128b+128) (reused for
+//       dQ^T); dV [256,384); dK [384,512). dS^T also goes to smem: B operand of dQ^T.
 // Masks: for partial tiles each lane builds 32-bit words "q row -> kv rows of my warp"
 // from the q rows' <= 2 attend ranges and transposes them across the warp (5 shuffles),
 // giving every kv-row thread a bitmask over its q columns; the element loop is branch-free.
@@ -37,10 +39,11 @@
 namespace dcpx {
 
 constexpr int kBwdThreads = 512;
-constexpr int kBwdStages = 4;
-// K 32K | V 32K | dS^T[2] 32K | stages[4] x (Q 16K | dO 16K) | LSE[4] 1K | Delta[4] 1K | barriers
+constexpr int kBwdStages = 3;
+// K 32K | V 32K | dS^T[2] 32K | stages[3] x (Q 16K | dO 16K) | dQ / dK / dV staging 32K |
+// LSE[3] 1K | Delta[3] 1K | barriers
 constexpr int kBwdStageBytes = 32768;
-constexpr int kBwdSmemMain = (96 + 32 * kBwdStages) * 1024;
+constexpr int kBwdSmemMain = (96 + 32 * kBwdStages + 32) * 1024;
 constexpr int kBwdSmem = kBwdSmemMain + 2048 + 256;
 static_assert(kBwdSmem <= 232448, "backward shared memory exceeds the sm_100 opt-in limit");
 
@@ -91,6 +94,8 @@ __device__ __forceinline__ uint32_t warp_transpose32(uint32_t x, int lane) {
     stmt;                                   \
     prof_[i] += clock64() - t_;             \
   } while (0)
+#define BWD_MARK(v) const long long v = clock64()
+#define BWD_ADD(i, t0) prof_[i] += clock64() - (t0)
 #define BWD_PROF_PRINT(name, a, b, c, d, e, f)                                                            \
   do {                                                                                                     \
     if (blockIdx.x == 0)                                                                                   \
@@ -100,6 +105,8 @@ __device__ __forceinline__ uint32_t warp_transpose32(uint32_t x, int lane) {
 #else
 #define BWD_PROF_DECL
 #define BWD_TIMED(i, stmt) stmt
+#define BWD_MARK(v)
+#define BWD_ADD(i, t0)
 #define BWD_PROF_PRINT(name, a, b, c, d, e, f) \
   do {                                         \
   } while (0)
@@ -108,12 +115,13 @@ __device__ __forceinline__ uint32_t warp_transpose32(uint32_t x, int lane) {
 __global__ void __launch_bounds__(kBwdThreads, 1)
     attn_bwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_do,
                     const __grid_constant__ CUtensorMap tm_kv, const __grid_constant__ CUtensorMap tm_dq,
-                    const BwdParams p) {
+                    const __grid_constant__ CUtensorMap tm_dkv, const BwdParams p) {
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* sK = smem;                 // [128 kv][128 d] as two SW128 halves of 64 d
   uint8_t* sV = smem + 32768;
   uint8_t* sDS = smem + 65536;        // [2][128 kv][64 q] bf16, SW128 rows of 128 B
-  uint8_t* sStage = smem + 98304;     // [4] x (Q [64 q][128 d] | dO [64 q][128 d]), halves of 64 d
+  uint8_t* sStage = smem + 98304;     // [3] x (Q [64 q][128 d] | dO [64 q][128 d]), halves of 64 d
+  uint8_t* sEpi = sStage + kBwdStages * kBwdStageBytes;  // staging: dQ [4][64 q][32] | dK/dV [2][128 kv][32] fp32
   float* sLSE = reinterpret_cast<float*>(smem + kBwdSmemMain);          // [4][64] (log2 units)
   float* sDelta = reinterpret_cast<float*>(smem + kBwdSmemMain + 1024);  // [4][64]
   BwdBarriers& bars = *reinterpret_cast<BwdBarriers*>(smem + kBwdSmemMain + 2048);
@@ -127,7 +135,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     mbar_init(&bars.kv_empty, 1);
     for (int i = 0; i < kBwdStages; ++i) {
       mbar_init(&bars.q_full[i], 1);
-      mbar_init(&bars.q_empty[i], 1);  // drain: dQ staged in the stage and read by TMA
+      mbar_init(&bars.q_empty[i], 1);  // MMA commit after dK, the stage's last reader
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&bars.s_full[b], 1);
@@ -137,12 +145,13 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       mbar_init(&bars.ds_free[b], 1);
     }
     mbar_init(&bars.acc_full, 1);
-    mbar_init(&bars.acc_empty, 256);
+    mbar_init(&bars.acc_empty, 128);  // drain warpgroup: dK / dV read out of TMEM
     fence_barrier_init();
     tma_prefetch_desc(&tm_q);
     tma_prefetch_desc(&tm_do);
     tma_prefetch_desc(&tm_kv);
     tma_prefetch_desc(&tm_dq);
+    tma_prefetch_desc(&tm_dkv);
   }
   if (warp == 1) tmem_alloc<512>(&bars.tmem_base);
   tc_fence_before();
@@ -152,22 +161,13 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   if (warp < 4) asm volatile("setmaxnreg.dec.sync.aligned.u32 72;");
 
   if (warp == 0) {
-    // ------------------------------------------------------------ producer
+    // ------------------------------------------------------------ Q / dO producer
     // converged warp, one elected lane issues (keeps the TMA operands in uniform registers)
     {
       BWD_PROF_DECL
-      uint32_t g = 0, it = 0;
-      for (int u = blockIdx.x; u < p.num_units; u += gridDim.x, ++it) {
+      uint32_t g = 0;
+      for (int u = blockIdx.x; u < p.num_units; u += gridDim.x) {
         const BwdUnit U = p.units[u];
-        BWD_TIMED(0, mbar_wait(&bars.kv_empty, (it & 1) ^ 1));
-        if (elect_one()) {
-          mbar_arrive_expect_tx(&bars.kv_full, 65536);
-          for (int h = 0; h < 2; ++h) {
-            tma_load_2d(&tm_kv, &bars.kv_full, sK + h * 16384, 64 * h, U.kv_row0);
-            tma_load_2d(&tm_kv, &bars.kv_full, sV + h * 16384, 64 * h, U.kv_row0 + p.slot_rows);
-          }
-        }
-        __syncwarp();
         for (int j = 0; j < U.step_count; ++j, ++g) {
           const BwdStep S = p.steps[U.step_begin + j];
           const int st = g % kBwdStages;
@@ -185,7 +185,28 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           __syncwarp();
         }
       }
-      if (lane == 0) BWD_PROF_PRINT("producer", "kv_empty", "q_empty", "-", "-", "-", "-");
+      if (lane == 0) BWD_PROF_PRINT("q-prod", "-", "q_empty", "-", "-", "-", "-");
+    }
+  } else if (warp == 2) {
+    // ------------------------------------------------------------ K / V producer
+    // separate from the Q / dO stream so a unit boundary (waiting for the previous
+    // unit's MMAs to release K and V) never stalls the Q / dO prefetch
+    {
+      BWD_PROF_DECL
+      uint32_t it = 0;
+      for (int u = blockIdx.x; u < p.num_units; u += gridDim.x, ++it) {
+        const int32_t kv_row0 = p.units[u].kv_row0;
+        BWD_TIMED(0, mbar_wait(&bars.kv_empty, (it & 1) ^ 1));
+        if (elect_one()) {
+          mbar_arrive_expect_tx(&bars.kv_full, 65536);
+          for (int h = 0; h < 2; ++h) {
+            tma_load_2d(&tm_kv, &bars.kv_full, sK + h * 16384, 64 * h, kv_row0);
+            tma_load_2d(&tm_kv, &bars.kv_full, sV + h * 16384, 64 * h, kv_row0 + p.slot_rows);
+          }
+        }
+        __syncwarp();
+      }
+      if (lane == 0) BWD_PROF_PRINT("kv-prod", "kv_empty", "-", "-", "-", "-", "-");
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
@@ -214,11 +235,12 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           for (int kk = 0; kk < 4; ++kk)
             umma_ts(tbase + 256, tbase + 128 * b + kk * 8, sdesc_sw128(sdo + kk * 2048, 8192, 1024), id_g,
                     (!first || kk > 0) ? 1u : 0u);
-          // dK += dS^T Q   (A = dS^T K-major; B = Q MN-major)
+          // dK += dS^T Q   (A = dS^T bf16 in TMEM slot cols [32,64); B = Q MN-major)
 #pragma unroll
           for (int kk = 0; kk < 4; ++kk)
-            umma_ss(tbase + 384, sdesc_sw128(sds + kk * 32, 16, 1024), sdesc_sw128(sq + kk * 2048, 8192, 1024),
-                    id_g, (!first || kk > 0) ? 1u : 0u);
+            umma_ts(tbase + 384, tbase + 128 * b + 32 + kk * 8, sdesc_sw128(sq + kk * 2048, 8192, 1024), id_g,
+                    (!first || kk > 0) ? 1u : 0u);
+          umma_commit(&bars.q_empty[st]);
           // dQ^T = K^T dS^T (A = K MN-major over d, B = dS^T MN-major over q; K = 128 kv) -> dP^T slot
 #pragma unroll
           for (int kk = 0; kk < 8; ++kk)
@@ -302,6 +324,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           m_next = p.items[s_next.item];
         }
         const uint32_t b = grp, st = gs % kBwdStages;
+        BWD_MARK(t_mask);
         // ---- mask bits over the 64 q columns: mb[h] bit i <-> q column 32h + i
         uint32_t mb[2];
         if (S.cls == kTilePartial) {
@@ -321,9 +344,11 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           for (int h = 0; h < 2; ++h) mb[h] = bits_in(0, S.n_q - 32 * h);
         }
         if (!kv_valid) mb[0] = mb[1] = 0u;
+        BWD_ADD(3, t_mask);
         BWD_TIMED(0, mbar_wait(&bars.s_full[b], (gs >> 1) & 1));
         tc_fence_after();
         if (gs >= 2) BWD_TIMED(1, mbar_wait(&bars.ds_free[b], ((gs >> 1) - 1) & 1));
+        BWD_MARK(t_math);
         const float4* lse4 = reinterpret_cast<const float4*>(sLSE + st * 64);
         const float4* dlt4 = reinterpret_cast<const float4*>(sDelta + st * 64);
         const uint32_t slot = lane_addr + 128 * b;
@@ -358,8 +383,10 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
             dk[2 * e4] = pack_bf16(sv[0], sv[1]);
             dk[2 * e4 + 1] = pack_bf16(sv[2], sv[3]);
           }
-          // P^T row j, q columns [32h, 32h+32) as bf16 pairs -> slot cols [16h, 16h+16)
+          // P^T / dS^T row j, q columns [32h, 32h+32) as bf16 pairs -> slot cols
+          // [16h, 16h+16) / [32+16h, 48+16h) (A operands of dV / dK)
           tmem_st16(slot + 16 * h, pk);
+          tmem_st16(slot + 32 + 16 * h, dk);
           // dS^T row j, q columns [32h, 32h+32): 16-byte chunks 4h..4h+3, 128B-swizzled
 #pragma unroll
           for (int q4 = 0; q4 < 4; ++q4) {
@@ -372,45 +399,31 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         fence_proxy_async_smem();
         tc_fence_before();
         mbar_arrive(&bars.p_ready[b]);
+        BWD_ADD(4, t_math);
       }
       g += U.step_count;
-      // ---- unit epilogue: group 0 adds dV [256,384), group 1 adds dK [384,512)
-      BWD_TIMED(2, mbar_wait(&bars.acc_full, it & 1));
-      tc_fence_after();
-      float* dst = p.dkv_acc + ((int64_t)U.kv_row0 + (grp == 0 ? p.slot_rows : 0) + j) * 128;
-      const uint32_t col = grp == 0 ? 256 : 384;
-#pragma unroll 1
-      for (int cc = 0; cc < 128; cc += 32) {
-        uint32_t r[32];
-        tmem_ld32(lane_addr + col + cc, r);
-        tmem_wait_ld();
-        if (kv_valid) {
-#pragma unroll
-          for (int e = 0; e < 32; e += 4) red_add_v4(dst + cc + e, r + e);
-        }
-      }
-      tc_fence_before();
-      mbar_arrive(&bars.acc_empty);
     }
-    if (lane == 0 && wq == 0) BWD_PROF_PRINT(grp ? "compute1" : "compute0", "s_full", "ds_free", "acc_full", "-", "-", "-");
+    if (lane == 0 && wq == 0) BWD_PROF_PRINT(grp ? "compute1" : "compute0", "s_full", "ds_free", "-", "mask", "math", "-");
   } else if (warp >= 12) {
-    // ------------------------------------------------------------ dQ drain warpgroup
+    // ------------------------------------------------------------ drain warpgroup
     // dQ^T of step g sits in slot g&1 cols [64,128) with TMEM lane = head dim d. Thread d
     // writes column d of four [64 q][32 d] fp32 chunks (128B-swizzled; chunk k = d / 32)
-    // into the step's own stage buffer (free: dq_full is committed after dV and dK), then
-    // one thread reduce-adds them into the dQ accumulator and hands the stage back.
+    // into the 32 KiB staging area, then one lane reduce-adds them into the dQ accumulator.
+    // At the end of a unit the same warps move dV and dK out of TMEM (TMEM lane = kv row)
+    // in [128 x 32] fp32 chunks through the staging area (two 16 KiB halves) into TMA
+    // reduce-adds, so the compute warpgroups go straight on to the next unit.
     asm volatile("setmaxnreg.dec.sync.aligned.u32 104;");
     const int wq = warp & 3;
+    const int j = (wq << 5) + lane;  // kv row of the dK / dV epilogue
     const uint32_t lane_addr = tbase + ((uint32_t)(wq * 32) << 16);
     const uint32_t gran = (uint32_t)(lane >> 2), sub = (uint32_t)(lane & 3) * 4;
     BWD_PROF_DECL
-    uint32_t g = 0;
-    for (int u = blockIdx.x; u < p.num_units; u += gridDim.x) {
+    uint32_t g = 0, it = 0;
+    for (int u = blockIdx.x; u < p.num_units; u += gridDim.x, ++it) {
       const BwdUnit U = p.units[u];
       for (int s = 0; s < U.step_count; ++s, ++g) {
         const int q_row0 = p.steps[U.step_begin + s].q_row0;
-        const uint32_t b = g & 1, st = g % kBwdStages;
-        uint8_t* stage = sStage + st * kBwdStageBytes;
+        const uint32_t b = g & 1;
         BWD_TIMED(0, mbar_wait(&bars.dq_full[b], (g >> 1) & 1));
         tc_fence_after();
         uint32_t v[2][32];
@@ -419,25 +432,73 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         tmem_wait_ld();
         tc_fence_before();
         mbar_arrive(&bars.dq_empty[b]);
-        uint8_t* chunk = stage + wq * 8192 + sub;
+        // the staging area is free once the previous reduce-adds have read it
+        if (wq == 0) {
+          if (elect_one()) BWD_TIMED(2, bulk_wait_read<0>());
+          __syncwarp();
+        }
+        BWD_TIMED(1, named_bar_sync(2, 128));
+        uint8_t* chunk = sEpi + wq * 8192 + sub;
 #pragma unroll
         for (int q = 0; q < 64; ++q)
           *reinterpret_cast<uint32_t*>(chunk + q * 128 + ((gran ^ (q & 7)) << 4)) = v[q >> 5][q & 31];
         fence_proxy_async_smem();
-        BWD_TIMED(1, named_bar_sync(2, 128));
-        if (wq == 0 && lane == 0) {
-          if (!(p.debug_flags & 1))
-            for (int k = 0; k < 4; ++k) tma_reduce_add_2d(&tm_dq, stage + k * 8192, 32 * k, q_row0);
-          bulk_commit();
-          BWD_TIMED(2, bulk_wait_read<0>());
-          mbar_arrive(&bars.q_empty[st]);
+        named_bar_sync(2, 128);
+        if (wq == 0) {
+          if (elect_one()) {
+            if (!(p.debug_flags & 1))
+              for (int k = 0; k < 4; ++k) tma_reduce_add_2d(&tm_dq, sEpi + k * 8192, 32 * k, q_row0);
+            bulk_commit();
+          }
+          __syncwarp();
         }
       }
+      // ---- unit epilogue: dV (TMEM cols [256,384)) and dK ([384,512)), 8 chunks of 32
+      BWD_TIMED(3, mbar_wait(&bars.acc_full, it & 1));
+      BWD_MARK(t_epi);
+      tc_fence_after();
+#pragma unroll 1
+      for (int c = 0; c < 8; ++c) {
+        uint32_t r[32];
+        tmem_ld32(lane_addr + 256 + 32 * c, r);
+        tmem_wait_ld();
+        if (c == 7) {
+          tc_fence_before();
+          mbar_arrive(&bars.acc_empty);
+        }
+        // staging half c&1 was last read by the reduce-add two chunks back (chunk 0:
+        // wait for everything, including the last step's dQ which used both halves)
+        if (wq == 0) {
+          if (elect_one()) {
+            if (c == 0) bulk_wait_read<0>();
+            else bulk_wait_read<1>();
+          }
+          __syncwarp();
+        }
+        named_bar_sync(2, 128);
+        uint8_t* row = sEpi + (c & 1) * 16384 + j * 128;
+#pragma unroll
+        for (int q4 = 0; q4 < 8; ++q4)
+          *reinterpret_cast<uint4*>(row + ((q4 ^ (j & 7)) << 4)) =
+              make_uint4(r[4 * q4], r[4 * q4 + 1], r[4 * q4 + 2], r[4 * q4 + 3]);
+        fence_proxy_async_smem();
+        named_bar_sync(2, 128);
+        if (wq == 0) {
+          if (elect_one()) {
+            tma_reduce_add_2d(&tm_dkv, sEpi + (c & 1) * 16384, 32 * (c & 3),
+                              U.kv_row0 + (c < 4 ? p.slot_rows : 0));
+            bulk_commit();
+          }
+          __syncwarp();
+        }
+      }
+      BWD_ADD(4, t_epi);
     }
-    if (wq == 0 && lane == 0) {
-      bulk_wait<0>();
-      BWD_PROF_PRINT("drain", "dq_full", "bar", "tma_read", "-", "-", "-");
+    if (wq == 0) {
+      if (elect_one()) bulk_wait<0>();
+      __syncwarp();
     }
+    if (wq == 0 && lane == 0) BWD_PROF_PRINT("drain", "dq_full", "bar", "tma_read", "acc_full", "epilogue", "-");
   }
   tc_fence_before();
   __syncthreads();
@@ -445,7 +506,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 }
 
 void launch_attn_bwd(const CUtensorMap& tm_q, const CUtensorMap& tm_do, const CUtensorMap& tm_kv,
-                     const CUtensorMap& tm_dq, const BwdParams& p, int grid, cudaStream_t stream) {
+                     const CUtensorMap& tm_dq, const CUtensorMap& tm_dkv, const BwdParams& p, int grid,
+                     cudaStream_t stream) {
   // the dynamic shared-memory opt-in is a per-device function attribute
   static uint64_t configured = 0;
   int dev = 0;
@@ -454,7 +516,7 @@ void launch_attn_bwd(const CUtensorMap& tm_q, const CUtensorMap& tm_do, const CU
     cudaFuncSetAttribute(attn_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kBwdSmem);
     configured |= 1ull << dev;
   }
-  attn_bwd_kernel<<<grid, kBwdThreads, kBwdSmem, stream>>>(tm_q, tm_do, tm_kv, tm_dq, p);
+  attn_bwd_kernel<<<grid, kBwdThreads, kBwdSmem, stream>>>(tm_q, tm_do, tm_kv, tm_dq, tm_dkv, p);
 }
 
 void set_watchdog_buffer_bwd(uint32_t* diag) {

@@ -74,13 +74,13 @@ CUtensorMap make_tmap(void* base, int64_t rows, uint32_t box_rows = 128) {
   return m;
 }
 
-// 2-D fp32 tensor map over a [rows][128] accumulator, box 64 rows x 32 columns (128 B),
-// 128-byte swizzle: the TMA reduce-add target of the backward's dQ drain.
-CUtensorMap make_tmap_f32(void* base, int64_t rows) {
+// 2-D fp32 tensor map over a [rows][128] accumulator, box `box_rows` rows x 32 columns
+// (128 B), 128-byte swizzle: the TMA reduce-add target of the backward's drain warps.
+CUtensorMap make_tmap_f32(void* base, int64_t rows, uint32_t box_rows) {
   CUtensorMap m;
   cuuint64_t dims[2] = {128, static_cast<cuuint64_t>(rows)};
   cuuint64_t strides[1] = {512};
-  cuuint32_t box[2] = {32, kBwdQRows};
+  cuuint32_t box[2] = {32, box_rows};
   cuuint32_t es[2] = {1, 1};
   CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, base, dims, strides, box, es,
                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -796,10 +796,11 @@ void Executor::compile_device(int d) {
     CUDA_OK(cudaMemset(D.lse2, 0, nq * SR * 4));
     CUDA_OK(cudaMemset(D.delta, 0, nq * SR * 4));
     D.tm_do = make_tmap(D.d_o, nq * SR, kBwdQRows);
-    D.tm_dq = make_tmap_f32(D.dq_acc, nq * SR);
+    D.tm_dq = make_tmap_f32(D.dq_acc, nq * SR, kBwdQRows);
     D.tm_q = make_tmap(D.q, std::max<int64_t>(1, D.cap_q) * SR);
     D.tm_q64 = make_tmap(D.q, std::max<int64_t>(1, D.cap_q) * SR, kBwdQRows);
     D.tm_kv = make_tmap(D.kv, std::max<int64_t>(1, D.cap_kv) * 2 * SR);
+    D.tm_dkv = make_tmap_f32(D.dkv_acc, nkv * 2 * SR, 128);
     std::vector<int32_t> ranges = g_.ranges;
     ranges.insert(ranges.end(), P.rows.begin(), P.rows.end());
     if (ranges.empty()) ranges.assign(4, 0);
@@ -1583,7 +1584,7 @@ void Executor::backward(const void* d_o, void* dq, void* dk, void* dv, dcpx_repo
           p.debug_flags = opt.bwd_debug;
           std::pair<cudaEvent_t, cudaEvent_t> ke{};
           if (opt.kernel_timing) { ke = kernel_events(d); CUDA_OK(cudaEventRecord(ke.first, D.cs)); }
-          launch_attn_bwd(D.tm_q64, D.tm_do, D.tm_kv, D.tm_dq, p, attn_grid(d, op.bgrid), D.cs);
+          launch_attn_bwd(D.tm_q64, D.tm_do, D.tm_kv, D.tm_dq, D.tm_dkv, p, attn_grid(d, op.bgrid), D.cs);
           if (opt.kernel_timing) CUDA_OK(cudaEventRecord(ke.second, D.cs));
           ++D.launches;
         }

@@ -48,7 +48,8 @@ void launch_accum(const DevJobs& j, const __nv_bfloat16* src, float* dst, cudaSt
 void launch_to_bf16(const DevJobs& j, const float* src, __nv_bfloat16* dst, cudaStream_t s);
 
 void launch_attn_bwd(const CUtensorMap& tm_q, const CUtensorMap& tm_do, const CUtensorMap& tm_kv,
-                     const CUtensorMap& tm_dq, const BwdParams& p, int grid, cudaStream_t stream);
+                     const CUtensorMap& tm_dq, const CUtensorMap& tm_dkv, const BwdParams& p, int grid,
+                     cudaStream_t stream);
 void set_watchdog_buffer_fwd(uint32_t* diag);  // per current device
 void set_watchdog_buffer_bwd(uint32_t* diag);
 void launch_attn_fwd(const CUtensorMap& tm_q, const CUtensorMap& tm_kv, const FwdParams& p, int grid,

@@ -75,6 +75,63 @@ __global__ void __launch_bounds__(128, 1) bench(int iters, long long* out) {
   if (threadIdx.x < 32) tmem_dealloc<512>(tbase);
 }
 
+// One backward step's MMA sequence (attn_bwd.cu): S^T, dP^T (N=64, K-major), dV (TS,
+// N=128, B MN-major), dK (SS, N=128, B MN-major), dQ^T (N=64, A and B MN-major).
+__global__ void __launch_bounds__(128, 1) bwd_mix(int steps, long long* out) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ uint64_t bar;
+  __shared__ uint32_t tbase_s;
+  for (int i = threadIdx.x; i < 160 * 1024 / 4; i += blockDim.x)
+    reinterpret_cast<uint32_t*>(smem)[i] = 0x3c003c00u ^ (i * 2654435761u & 0x00ff00ffu);
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    fence_barrier_init();
+  }
+  if (threadIdx.x < 32) tmem_alloc<512>(&tbase_s);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = tbase_s;
+  if (threadIdx.x < 32) {
+    fence_proxy_async_smem();
+    constexpr uint32_t id_s = idesc_bf16_f32(128, 64, 0, 0), id_g = idesc_bf16_f32(128, 128, 0, 1),
+                       id_q = idesc_bf16_f32(128, 64, 1, 1);
+    const uint32_t sk = smem_u32(smem), sv = sk + 32768, sds0 = sk + 65536, sst = sk + 98304;
+    const long long t0 = clock64();
+    for (int g = 0; g < steps; ++g) {
+      const uint32_t b = g & 1, sq = sst + (g % 2) * 32768, sdo = sq + 16384, sds = sds0 + b * 16384;
+      if (elect_one()) {
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk)
+          umma_ss(tbase + 128 * b, sdesc_sw128(sk + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024),
+                  sdesc_sw128(sq + (kk >> 2) * 8192 + (kk & 3) * 32, 16, 1024), id_s, kk > 0);
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk)
+          umma_ss(tbase + 128 * b + 64, sdesc_sw128(sv + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024),
+                  sdesc_sw128(sdo + (kk >> 2) * 8192 + (kk & 3) * 32, 16, 1024), id_s, kk > 0);
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)
+          umma_ts(tbase + 256, tbase + 128 * (b ^ 1) + kk * 8, sdesc_sw128(sdo + kk * 2048, 8192, 1024), id_g, 1);
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)
+          umma_ss(tbase + 384, sdesc_sw128(sds + kk * 32, 16, 1024), sdesc_sw128(sq + kk * 2048, 8192, 1024), id_g, 1);
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk)
+          umma_ss(tbase + 128 * (b ^ 1) + 64, sdesc_sw128(sk + kk * 2048, 16384, 1024),
+                  sdesc_sw128(sds + kk * 2048, 8192, 1024), id_q, kk > 0);
+      }
+      __syncwarp();
+    }
+    if (elect_one()) umma_commit(&bar);
+    __syncwarp();
+    mbar_wait(&bar, 0);
+    if (blockIdx.x == 0 && threadIdx.x == 0) out[0] = clock64() - t0;
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (threadIdx.x < 32) tmem_dealloc<512>(tbase);
+}
+
 template <int N, int AMN, int BMN, bool TS, int NACC, bool WARP>
 void run(const char* name, long long* d_out, int sms) {
   auto k = bench<N, AMN, BMN, TS, NACC, WARP>;
@@ -123,5 +180,12 @@ int main() {
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   all<false>(d_out, sms);
   all<true>(d_out, sms);
+  cudaFuncSetAttribute(bwd_mix, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+  const int steps = 2048;
+  for (int rep = 0; rep < 3; ++rep) bwd_mix<<<sms, 128, 160 * 1024>>>(steps, d_out);
+  cudaDeviceSynchronize();
+  long long cyc = 0;
+  cudaMemcpy(&cyc, d_out, 8, cudaMemcpyDeviceToHost);
+  printf("backward step MMA mix: %.0f cyc/step (32 MMAs; 24 x N=64 + 8 x N=128)\n", (double)cyc / steps);
   return 0;
 }
