@@ -211,12 +211,23 @@ def main():
     ex = DCPExecutor(list(range(N)))
     ex.set_option("kernel_timing", 1)
     ex.prepare(bundle)
+    # N > 1: the distributed layout (dcpx_*_dev) -- every GPU holds the packed Q/K/V/dO of
+    # the batch in its own HBM and receives the output rows it owns, as in a training step
+    # where each GPU produced its own tokens; no input or output crosses NVLink.
+    if N > 1:
+        def per_dev(x, like=False):
+            return [torch.empty_like(x, device=f"cuda:{d}") if like else x.to(f"cuda:{d}") for d in range(N)]
+        io = dict(q=per_dev(q), k=per_dev(k), v=per_dev(v), d_o=per_dev(d_o), o=per_dev(o, True),
+                  lse=per_dev(lse, True), dq=per_dev(dq, True), dk=per_dev(dk, True), dv=per_dev(dv, True))
+    else:
+        io = dict(q=q, k=k, v=v, d_o=d_o, o=o, lse=lse, dq=dq, dk=dk, dv=dv)
+    config["io_layout"] = "per-device packed buffers (dcpx_*_dev)" if N > 1 else "packed buffers on cuda:0"
     barrier()
 
     def step():
-        ex.load_inputs(q, k, v)
-        rf = ex.forward(o, lse)
-        rb = ex.backward(d_o, dq, dk, dv)
+        ex.load_inputs(io["q"], io["k"], io["v"])
+        rf = ex.forward(io["o"], io["lse"])
+        rb = ex.backward(io["d_o"], io["dq"], io["dk"], io["dv"])
         return rf, rb
 
     for _ in range(args.warmup):

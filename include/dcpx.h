@@ -183,8 +183,9 @@ dcpx_status dcpx_prepare(dcpx_ctx* ctx, int nplans, const dcpx_plan_view* plans,
                          const dcpx_graph_view* graph, const dcpx_mask_view* masks);
 
 /* Packed bf16 inputs on the context's device(s): q [T][H][D], k, v [T][G][D].
- * In LOCAL mode with several GPUs, pointers refer to cuda_ordinals[0]'s memory and
- * are copied peer-to-peer to the owners. Scatters rows into the resident slots. */
+ * In LOCAL mode with several GPUs, every device reads its resident rows from this one
+ * buffer (peer-to-peer when it lives on another GPU; see dcpx_load_inputs_dev for the
+ * distributed layout). Scatters rows into the resident slots. */
 dcpx_status dcpx_load_inputs(dcpx_ctx* ctx, const void* q, const void* k, const void* v);
 /* Same with host (pinned or pageable) pointers; host->device copies are inside. */
 dcpx_status dcpx_load_inputs_host(dcpx_ctx* ctx, const void* q, const void* k, const void* v);
@@ -200,6 +201,18 @@ dcpx_status dcpx_backward(dcpx_ctx* ctx, const void* d_o, void* dq, void* dk, vo
                           dcpx_report* rep);
 dcpx_status dcpx_backward_host(dcpx_ctx* ctx, const void* d_o, void* dq, void* dk, void* dv,
                                dcpx_report* rep);
+
+/* Distributed layout (no reference counterpart: the reference's payload is one host
+ * object). Entry d of every array is a packed buffer of the single-buffer calls' shape in
+ * plan device d's own memory; device d reads only the input rows of the blocks resident
+ * on it and writes only the output rows it owns, so no input or output crosses NVLink.
+ * This is the layout a training step has, where each GPU produced its own tokens' Q/K/V.
+ * Output arrays (or their entries) may be NULL to skip that output. */
+dcpx_status dcpx_load_inputs_dev(dcpx_ctx* ctx, const void* const* q, const void* const* k,
+                                 const void* const* v);
+dcpx_status dcpx_forward_dev(dcpx_ctx* ctx, void* const* o_out, float* const* lse_out, dcpx_report* rep);
+dcpx_status dcpx_backward_dev(dcpx_ctx* ctx, const void* const* d_o, void* const* dq, void* const* dk,
+                              void* const* dv, dcpx_report* rep);
 
 /* Synchronises all streams of the context. */
 dcpx_status dcpx_synchronize(dcpx_ctx* ctx);

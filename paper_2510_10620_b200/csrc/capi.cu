@@ -29,6 +29,12 @@ dcpx_status guarded(dcpx_ctx* ctx, F&& f) {
     return DCPX_ERROR;
   }
 }
+// single-buffer calls: every plan device reads / writes the same packed buffer
+template <class T>
+std::vector<T> same_for_all(const dcpx::Executor& ex, T p) {
+  return std::vector<T>(static_cast<size_t>(std::max(1, ex.devices())), p);
+}
+
 }  // namespace
 
 extern "C" {
@@ -62,19 +68,38 @@ dcpx_status dcpx_prepare(dcpx_ctx* ctx, int nplans, const dcpx_plan_view* plans,
 }
 
 dcpx_status dcpx_load_inputs(dcpx_ctx* ctx, const void* q, const void* k, const void* v) {
-  return guarded(ctx, [&](dcpx::Executor& ex) { ex.load_inputs(q, k, v, false); });
+  return guarded(ctx, [&](dcpx::Executor& ex) {
+    ex.load_inputs(same_for_all(ex, q).data(), same_for_all(ex, k).data(), same_for_all(ex, v).data(), false);
+  });
 }
 
 dcpx_status dcpx_load_inputs_host(dcpx_ctx* ctx, const void* q, const void* k, const void* v) {
-  return guarded(ctx, [&](dcpx::Executor& ex) { ex.load_inputs(q, k, v, true); });
+  return guarded(ctx, [&](dcpx::Executor& ex) {
+    ex.load_inputs(same_for_all(ex, q).data(), same_for_all(ex, k).data(), same_for_all(ex, v).data(), true);
+  });
+}
+
+dcpx_status dcpx_load_inputs_dev(dcpx_ctx* ctx, const void* const* q, const void* const* k, const void* const* v) {
+  return guarded(ctx, [&](dcpx::Executor& ex) {
+    if (!q || !k || !v) throw dcpx::Failure(DCPX_ERROR, "dcpx_load_inputs_dev: null pointer array");
+    ex.load_inputs(q, k, v, false);
+  });
 }
 
 dcpx_status dcpx_forward(dcpx_ctx* ctx, void* o_out, float* lse_out, dcpx_report* rep) {
+  return guarded(ctx, [&](dcpx::Executor& ex) {
+    ex.forward(same_for_all(ex, o_out).data(), same_for_all(ex, lse_out).data(), rep, false);
+  });
+}
+
+dcpx_status dcpx_forward_dev(dcpx_ctx* ctx, void* const* o_out, float* const* lse_out, dcpx_report* rep) {
   return guarded(ctx, [&](dcpx::Executor& ex) { ex.forward(o_out, lse_out, rep, false); });
 }
 
 dcpx_status dcpx_forward_host(dcpx_ctx* ctx, void* o_out, float* lse_out, dcpx_report* rep) {
-  return guarded(ctx, [&](dcpx::Executor& ex) { ex.forward(o_out, lse_out, rep, true); });
+  return guarded(ctx, [&](dcpx::Executor& ex) {
+    ex.forward(same_for_all(ex, o_out).data(), same_for_all(ex, lse_out).data(), rep, true);
+  });
 }
 
 dcpx_status dcpx_synchronize(dcpx_ctx* ctx) {
@@ -133,9 +158,23 @@ dcpx_status dcpx_create_rank(int, int, int, const void*, dcpx_ctx** out) {
 }
 dcpx_status dcpx_nccl_unique_id(void*) { return DCPX_UNSUPPORTED; }
 dcpx_status dcpx_backward(dcpx_ctx* ctx, const void* d_o, void* dq, void* dk, void* dv, dcpx_report* rep) {
-  return guarded(ctx, [&](dcpx::Executor& ex) { ex.backward(d_o, dq, dk, dv, rep, false); });
+  return guarded(ctx, [&](dcpx::Executor& ex) {
+    ex.backward(same_for_all(ex, d_o).data(), same_for_all(ex, dq).data(), same_for_all(ex, dk).data(),
+                same_for_all(ex, dv).data(), rep, false);
+  });
+}
+
+dcpx_status dcpx_backward_dev(dcpx_ctx* ctx, const void* const* d_o, void* const* dq, void* const* dk,
+                              void* const* dv, dcpx_report* rep) {
+  return guarded(ctx, [&](dcpx::Executor& ex) {
+    if (!d_o) throw dcpx::Failure(DCPX_ERROR, "dcpx_backward_dev: null d_o array");
+    ex.backward(d_o, dq, dk, dv, rep, false);
+  });
 }
 dcpx_status dcpx_backward_host(dcpx_ctx* ctx, const void* d_o, void* dq, void* dk, void* dv, dcpx_report* rep) {
-  return guarded(ctx, [&](dcpx::Executor& ex) { ex.backward(d_o, dq, dk, dv, rep, true); });
+  return guarded(ctx, [&](dcpx::Executor& ex) {
+    ex.backward(same_for_all(ex, d_o).data(), same_for_all(ex, dq).data(), same_for_all(ex, dk).data(),
+                same_for_all(ex, dv).data(), rep, true);
+  });
 }
 }

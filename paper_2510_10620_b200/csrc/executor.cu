@@ -251,7 +251,7 @@ void Executor::trace_begin() {
 
 TraceScope::TraceScope(Executor* ex, int d, int instr, cudaStream_t s, int pass, const Op& op)
     : ex_(ex), d_(d) {
-  if (!ex->opt.trace || op.kind == OpKind::kNop || op.kind == OpKind::kCommLaunch) return;
+  if (!ex->opt.trace || op.kind == OpKind::kNop) return;
   auto ev = ex->kernel_events(d);
   CUDA_OK(cudaEventRecord(ev.first, s));
   ex->trace_pending_.push_back({d, instr, static_cast<int>(op.kind), op.division, pass, ev.first, ev.second});
@@ -261,6 +261,15 @@ TraceScope::TraceScope(Executor* ex, int d, int instr, cudaStream_t s, int pass,
 
 TraceScope::~TraceScope() {
   if (active_) cudaEventRecord(ex_->trace_pending_.back().end, s_);
+}
+
+void TraceScope::split(int kind) {
+  if (!active_) return;
+  auto ev = ex_->kernel_events(d_);
+  CUDA_OK(cudaEventRecord(ev.first, s_));
+  Executor::TracePending prev = ex_->trace_pending_.back();
+  ex_->trace_pending_.back().end = ev.first;
+  ex_->trace_pending_.push_back({prev.d, prev.instr, kind, prev.division, prev.pass, ev.first, ev.second});
 }
 
 void Executor::trace_collect() {
@@ -1287,10 +1296,10 @@ void Executor::build_bwd_jobs() {
 }
 
 // ------------------------------------------------------------------------ execution
-void Executor::load_inputs(const void* q, const void* k, const void* v, bool host) {
+void Executor::load_inputs(const void* const* q, const void* const* k, const void* const* v, bool host) {
   if (!prepared_) throw Failure(DCPX_ERROR, "dcpx_load_inputs before dcpx_prepare");
   const int64_t TT = g_.total_tokens();
-  const void *dq = q, *dk = k, *dv = v;
+  std::vector<const void*> sq(q, q + R_), sk(k, k + R_), sv(v, v + R_);
   if (host) {
     // stage once on the first device; peers read it over NVLink
     DevState& D0 = dev_[0];
@@ -1298,28 +1307,30 @@ void Executor::load_inputs(const void* q, const void* k, const void* v, bool hos
     const size_t bq = TT * g_.H * 256, bk = TT * g_.G * 256;
     if (!in_stage_) in_stage_ = static_cast<char*>(alloc(0, bq + 2 * bk));
     char* buf = in_stage_;
-    CUDA_OK(cudaMemcpyAsync(buf, q, bq, cudaMemcpyHostToDevice, D0.cs));
-    CUDA_OK(cudaMemcpyAsync(buf + bq, k, bk, cudaMemcpyHostToDevice, D0.cs));
-    CUDA_OK(cudaMemcpyAsync(buf + bq + bk, v, bk, cudaMemcpyHostToDevice, D0.cs));
+    CUDA_OK(cudaMemcpyAsync(buf, q[0], bq, cudaMemcpyHostToDevice, D0.cs));
+    CUDA_OK(cudaMemcpyAsync(buf + bq, k[0], bk, cudaMemcpyHostToDevice, D0.cs));
+    CUDA_OK(cudaMemcpyAsync(buf + bq + bk, v[0], bk, cudaMemcpyHostToDevice, D0.cs));
     cudaEvent_t e = event(0);
     CUDA_OK(cudaEventRecord(e, D0.cs));
     for (int d = 1; d < R_; ++d) {
       DeviceGuard g2(dev_[d].ordinal);
       CUDA_OK(cudaStreamWaitEvent(dev_[d].cs, e, 0));
     }
-    dq = buf; dk = buf + bq; dv = buf + bq + bk;
+    std::fill(sq.begin(), sq.end(), buf);
+    std::fill(sk.begin(), sk.end(), buf + bq);
+    std::fill(sv.begin(), sv.end(), buf + bq + bk);
   }
   for (int d = 0; d < R_; ++d) {
     DevState& D = dev_[d];
     DeviceGuard gd(D.ordinal);
-    launch_row_copy(D.scatter_q.dj, D.cs, reinterpret_cast<int64_t>(dq), 0);
-    launch_row_copy(D.scatter_k.dj, D.cs, reinterpret_cast<int64_t>(dk), 0);
-    launch_row_copy(D.scatter_v.dj, D.cs, reinterpret_cast<int64_t>(dv), 0);
+    launch_row_copy(D.scatter_q.dj, D.cs, reinterpret_cast<int64_t>(sq[d]), 0);
+    launch_row_copy(D.scatter_k.dj, D.cs, reinterpret_cast<int64_t>(sk[d]), 0);
+    launch_row_copy(D.scatter_v.dj, D.cs, reinterpret_cast<int64_t>(sv[d]), 0);
     CUDA_OK(cudaGetLastError());
   }
 }
 
-void Executor::forward(void* o_out, float* lse_out, dcpx_report* rep, bool host) {
+void Executor::forward(void* const* o_out, float* const* lse_out, dcpx_report* rep, bool host) {
   if (!prepared_) throw Failure(DCPX_ERROR, "dcpx_forward before dcpx_prepare");
   const int64_t TT = g_.total_tokens();
   for (auto& D : dev_) {
@@ -1378,6 +1389,7 @@ void Executor::forward(void* o_out, float* lse_out, dcpx_report* rep, bool host)
       case OpKind::kCommWait: {
         CUDA_OK(cudaStreamWaitEvent(D.ms, send_ev.at(op.tag), 0));
         CUDA_OK(cudaStreamWaitEvent(D.ms, recv_ev.at(op.tag), 0));
+        ts.split(kTraceXfer);
         if (opt.sm_transfers) {
           launch_row_copy(op.jobs.dj, D.ms);
           ++D.launches;
@@ -1394,23 +1406,26 @@ void Executor::forward(void* o_out, float* lse_out, dcpx_report* rep, bool host)
     }
   }
   // output assembly (simexec.hpp:403-421) into the caller's packed buffers
-  char* o_dev = static_cast<char*>(o_out);
-  char* l_dev = reinterpret_cast<char*>(lse_out);
-  if (host && (o_out || lse_out)) {
+  std::vector<char*> o_dev(static_cast<size_t>(R_)), l_dev(static_cast<size_t>(R_));
+  for (int d = 0; d < R_; ++d) {
+    o_dev[d] = static_cast<char*>(o_out ? o_out[d] : nullptr);
+    l_dev[d] = reinterpret_cast<char*>(lse_out ? lse_out[d] : nullptr);
+  }
+  const bool want_o = o_dev[0] != nullptr, want_l = l_dev[0] != nullptr;
+  if (host && (want_o || want_l)) {
     if (!out_stage_) out_stage_ = static_cast<char*>(alloc(0, TT * g_.H * 256 + TT * g_.H * 4));
-    char* buf = out_stage_;
-    o_dev = o_out ? buf : nullptr;
-    l_dev = lse_out ? buf + TT * g_.H * 256 : nullptr;
+    std::fill(o_dev.begin(), o_dev.end(), want_o ? out_stage_ : nullptr);
+    std::fill(l_dev.begin(), l_dev.end(), want_l ? out_stage_ + TT * g_.H * 256 : nullptr);
   }
   for (int d = 0; d < R_; ++d) {
     DevState& D = dev_[d];
     DeviceGuard gd(D.ordinal);
-    if (o_dev) { launch_row_copy(D.gather_o.dj, D.cs, 0, reinterpret_cast<int64_t>(o_dev)); ++D.launches; }
-    if (l_dev) { launch_row_copy(D.gather_lse.dj, D.cs, 0, reinterpret_cast<int64_t>(l_dev)); ++D.launches; }
+    if (o_dev[d]) { launch_row_copy(D.gather_o.dj, D.cs, 0, reinterpret_cast<int64_t>(o_dev[d])); ++D.launches; }
+    if (l_dev[d]) { launch_row_copy(D.gather_lse.dj, D.cs, 0, reinterpret_cast<int64_t>(l_dev[d])); ++D.launches; }
     if (opt.timing) CUDA_OK(cudaEventRecord(D.t1, D.cs));
     CUDA_OK(cudaGetLastError());
   }
-  if (host && (o_out || lse_out)) {
+  if (host && (want_o || want_l)) {
     DevState& D0 = dev_[0];
     DeviceGuard gd(D0.ordinal);
     for (int d = 1; d < R_; ++d) {
@@ -1420,8 +1435,8 @@ void Executor::forward(void* o_out, float* lse_out, dcpx_report* rep, bool host)
       DeviceGuard g3(D0.ordinal);
       CUDA_OK(cudaStreamWaitEvent(D0.cs, e, 0));
     }
-    if (o_out) CUDA_OK(cudaMemcpyAsync(o_out, o_dev, TT * g_.H * 256, cudaMemcpyDeviceToHost, D0.cs));
-    if (lse_out) CUDA_OK(cudaMemcpyAsync(lse_out, l_dev, TT * g_.H * 4, cudaMemcpyDeviceToHost, D0.cs));
+    if (want_o) CUDA_OK(cudaMemcpyAsync(o_out[0], o_dev[0], TT * g_.H * 256, cudaMemcpyDeviceToHost, D0.cs));
+    if (want_l) CUDA_OK(cudaMemcpyAsync(lse_out[0], l_dev[0], TT * g_.H * 4, cudaMemcpyDeviceToHost, D0.cs));
     CUDA_OK(cudaStreamSynchronize(D0.cs));
   }
   fill_report(rep, false);
@@ -1500,13 +1515,20 @@ void Executor::fill_report(dcpx_report* rep, bool bwd) {
   }
 }
 
-void Executor::backward(const void* d_o, void* dq, void* dk, void* dv, dcpx_report* rep, bool host) {
+void Executor::backward(const void* const* d_o, void* const* dq, void* const* dk, void* const* dv,
+                        dcpx_report* rep, bool host) {
   if (!prepared_) throw Failure(DCPX_ERROR, "dcpx_backward before dcpx_prepare");
   if (!fwd_done_) throw Failure(DCPX_ERROR, "dcpx_backward needs a preceding dcpx_forward");
   const int64_t TT = g_.total_tokens(), H = g_.H, G = g_.G;
   const int T = R_ ? plans_[0].divisions : 0;
-  const char* ddo = static_cast<const char*>(d_o);
-  char *ddq = static_cast<char*>(dq), *ddk = static_cast<char*>(dk), *ddv = static_cast<char*>(dv);
+  std::vector<const char*> ddo(static_cast<size_t>(R_));
+  std::vector<char*> ddq(static_cast<size_t>(R_)), ddk(static_cast<size_t>(R_)), ddv(static_cast<size_t>(R_));
+  for (int d = 0; d < R_; ++d) {
+    ddo[d] = static_cast<const char*>(d_o[d]);
+    ddq[d] = static_cast<char*>(dq ? dq[d] : nullptr);
+    ddk[d] = static_cast<char*>(dk ? dk[d] : nullptr);
+    ddv[d] = static_cast<char*>(dv ? dv[d] : nullptr);
+  }
   const size_t bq = TT * H * 256, bk = TT * G * 256;
   for (auto& D : dev_) {
     D.next_event = 0;
@@ -1519,17 +1541,17 @@ void Executor::backward(const void* d_o, void* dq, void* dk, void* dv, dcpx_repo
     DevState& D0 = dev_[0];
     DeviceGuard gd(D0.ordinal);
     if (!bwd_stage_) bwd_stage_ = static_cast<char*>(alloc(0, 2 * bq + 2 * bk));
-    CUDA_OK(cudaMemcpyAsync(bwd_stage_, d_o, bq, cudaMemcpyHostToDevice, D0.cs));
+    CUDA_OK(cudaMemcpyAsync(bwd_stage_, d_o[0], bq, cudaMemcpyHostToDevice, D0.cs));
     cudaEvent_t e = event(0);
     CUDA_OK(cudaEventRecord(e, D0.cs));
     for (int d = 1; d < R_; ++d) {
       DeviceGuard g2(dev_[d].ordinal);
       CUDA_OK(cudaStreamWaitEvent(dev_[d].cs, e, 0));
     }
-    ddo = bwd_stage_;
-    ddq = bwd_stage_ + bq;
-    ddk = bwd_stage_ + 2 * bq;
-    ddv = bwd_stage_ + 2 * bq + bk;
+    std::fill(ddo.begin(), ddo.end(), bwd_stage_);
+    std::fill(ddq.begin(), ddq.end(), ddq[0] ? bwd_stage_ + bq : nullptr);
+    std::fill(ddk.begin(), ddk.end(), ddk[0] ? bwd_stage_ + 2 * bq : nullptr);
+    std::fill(ddv.begin(), ddv.end(), ddv[0] ? bwd_stage_ + 2 * bq + bk : nullptr);
   }
   const float scale = static_cast<float>(1.0 / std::sqrt(static_cast<double>(g_.D)));
   for (int d = 0; d < R_; ++d) {
@@ -1538,25 +1560,26 @@ void Executor::backward(const void* d_o, void* dq, void* dk, void* dv, dcpx_repo
     const int64_t SR = D.slot_rows;
     CUDA_OK(cudaMemsetAsync(D.dq_acc, 0, std::max<int64_t>(1, D.cap_q) * SR * 512, D.cs));
     CUDA_OK(cudaMemsetAsync(D.dkv_acc, 0, std::max<int64_t>(1, D.cap_kv) * 2 * SR * 512, D.cs));
-    launch_row_copy(D.scatter_do.dj, D.cs, reinterpret_cast<int64_t>(ddo), 0);
+    launch_row_copy(D.scatter_do.dj, D.cs, reinterpret_cast<int64_t>(ddo[d]), 0);
     launch_delta(D.prep.dj, D.o, D.lse, D.d_o, D.delta, D.lse2, D.cs);
     D.launches += 2;
   }
-  // every device's accumulators are zeroed before any peer returns into them
-  {
-    std::vector<cudaEvent_t> ev(static_cast<size_t>(R_));
-    for (int d = 0; d < R_; ++d) {
-      DeviceGuard gd(dev_[d].ordinal);
-      ev[d] = event(d);
-      CUDA_OK(cudaEventRecord(ev[d], dev_[d].cs));
-    }
-    for (int d = 0; d < R_; ++d)
-      for (int e = 0; e < R_; ++e)
-        if (e != d) {
-          DeviceGuard gd(dev_[d].ordinal);
-          CUDA_OK(cudaStreamWaitEvent(dev_[d].cs, ev[e], 0));
-        }
+  // every device's accumulators are zeroed before any peer returns into them: a device's
+  // first gradient return waits for its peers' zeroing (not its attention)
+  std::vector<cudaEvent_t> zeroed(static_cast<size_t>(R_));
+  std::vector<char> zero_waited(static_cast<size_t>(R_), 0);
+  for (int d = 0; d < R_; ++d) {
+    DeviceGuard gd(dev_[d].ordinal);
+    zeroed[d] = event(d);
+    CUDA_OK(cudaEventRecord(zeroed[d], dev_[d].cs));
   }
+  auto await_zeroed = [&](int d) {
+    if (zero_waited[d]) return;
+    zero_waited[d] = 1;
+    DeviceGuard gd(dev_[d].ordinal);
+    for (int e = 0; e < R_; ++e)
+      if (e != d) CUDA_OK(cudaStreamWaitEvent(dev_[d].cs, zeroed[e], 0));
+  };
   std::map<std::string, cudaEvent_t> send_ev, recv_ev;
   std::vector<cudaEvent_t> ready_ev(static_cast<size_t>(R_));
   for (int d = 0; d < R_; ++d) {  // dO scattered, Delta / LSE prepared on cs
@@ -1589,6 +1612,7 @@ void Executor::backward(const void* d_o, void* dq, void* dk, void* dv, dcpx_repo
           ++D.launches;
         }
         if (op.ret.dj.n_blocks) {
+          await_zeroed(d);
           launch_return_accum(op.ret.dj, D.cs);
           ++D.launches;
         }
@@ -1607,6 +1631,7 @@ void Executor::backward(const void* d_o, void* dq, void* dk, void* dv, dcpx_repo
       case OpKind::kCommWait: {
         CUDA_OK(cudaStreamWaitEvent(D.ms, send_ev.at(op.tag), 0));
         CUDA_OK(cudaStreamWaitEvent(D.ms, recv_ev.at(op.tag), 0));
+        ts.split(kTraceXfer);
         if (opt.sm_transfers) {
           launch_row_copy(op.bjobs.dj, D.ms);
           ++D.launches;
@@ -1640,9 +1665,9 @@ void Executor::backward(const void* d_o, void* dq, void* dk, void* dv, dcpx_repo
   for (int d = 0; d < R_; ++d) {
     DevState& D = dev_[d];
     DeviceGuard gd(D.ordinal);
-    if (ddq) { launch_to_bf16(D.gather_dq.dj, D.dq_acc, reinterpret_cast<__nv_bfloat16*>(ddq), D.cs); ++D.launches; }
-    if (ddk) { launch_to_bf16(D.gather_dk.dj, D.dkv_acc, reinterpret_cast<__nv_bfloat16*>(ddk), D.cs); ++D.launches; }
-    if (ddv) { launch_to_bf16(D.gather_dv.dj, D.dkv_acc, reinterpret_cast<__nv_bfloat16*>(ddv), D.cs); ++D.launches; }
+    if (ddq[d]) { launch_to_bf16(D.gather_dq.dj, D.dq_acc, reinterpret_cast<__nv_bfloat16*>(ddq[d]), D.cs); ++D.launches; }
+    if (ddk[d]) { launch_to_bf16(D.gather_dk.dj, D.dkv_acc, reinterpret_cast<__nv_bfloat16*>(ddk[d]), D.cs); ++D.launches; }
+    if (ddv[d]) { launch_to_bf16(D.gather_dv.dj, D.dkv_acc, reinterpret_cast<__nv_bfloat16*>(ddv[d]), D.cs); ++D.launches; }
     if (opt.timing) CUDA_OK(cudaEventRecord(D.t1, D.cs));
     CUDA_OK(cudaGetLastError());
   }
@@ -1658,9 +1683,9 @@ void Executor::backward(const void* d_o, void* dq, void* dk, void* dv, dcpx_repo
       CUDA_OK(cudaStreamWaitEvent(D0.cs, e, 0));
     }
     DeviceGuard gd(D0.ordinal);
-    if (dq) CUDA_OK(cudaMemcpyAsync(dq, ddq, bq, cudaMemcpyDeviceToHost, D0.cs));
-    if (dk) CUDA_OK(cudaMemcpyAsync(dk, ddk, bk, cudaMemcpyDeviceToHost, D0.cs));
-    if (dv) CUDA_OK(cudaMemcpyAsync(dv, ddv, bk, cudaMemcpyDeviceToHost, D0.cs));
+    if (ddq[0]) CUDA_OK(cudaMemcpyAsync(dq[0], ddq[0], bq, cudaMemcpyDeviceToHost, D0.cs));
+    if (ddk[0]) CUDA_OK(cudaMemcpyAsync(dk[0], ddk[0], bk, cudaMemcpyDeviceToHost, D0.cs));
+    if (ddv[0]) CUDA_OK(cudaMemcpyAsync(dv[0], ddv[0], bk, cudaMemcpyDeviceToHost, D0.cs));
     CUDA_OK(cudaStreamSynchronize(D0.cs));
   }
   fill_report(rep, true);

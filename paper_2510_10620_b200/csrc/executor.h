@@ -57,6 +57,7 @@ struct JobList {
 };
 
 enum class OpKind { kFwdAttn, kMerge, kCopy, kCommLaunch, kCommWait, kNop };
+constexpr int kTraceXfer = 6;  // trace-only kind: the transfer part of a comm wait
 
 struct Op {
   OpKind kind = OpKind::kNop;
@@ -137,6 +138,9 @@ class TraceScope {
  public:
   TraceScope(Executor* ex, int d, int instr, cudaStream_t s, int pass, const Op& op);
   ~TraceScope();
+  // Ends the current span here and opens a second one of trace kind `kind` (e.g. a
+  // comm wait's transfer once its events have resolved).
+  void split(int kind);
 
  private:
   Executor* ex_;
@@ -151,9 +155,15 @@ class Executor {
   ~Executor();
   void prepare(int nplans, const dcpx_plan_view* plans, const dcpx_graph_view* g,
                const dcpx_mask_view* m);
-  void load_inputs(const void* q, const void* k, const void* v, bool host);
-  void forward(void* o_out, float* lse_out, dcpx_report* rep, bool host);
-  void backward(const void* d_o, void* dq, void* dk, void* dv, dcpx_report* rep, bool host);
+  int devices() const { return R_; }  // plan devices (0 before prepare)
+  // Packed I/O buffers, one pointer per plan device: device d reads / writes only the rows
+  // of the blocks it owns. The single-buffer API passes the same buffer for every device;
+  // the per-device (_dev) API passes buffers in each device's own memory. host: all
+  // entries are one host buffer, staged through the first device.
+  void load_inputs(const void* const* q, const void* const* k, const void* const* v, bool host);
+  void forward(void* const* o_out, float* const* lse_out, dcpx_report* rep, bool host);
+  void backward(const void* const* d_o, void* const* dq, void* const* dk, void* const* dv, dcpx_report* rep,
+                bool host);
   void synchronize();
   void debug_arena(int dev, int kind, void** ptr, int64_t* rows);
   int trace_rows(double* out, int max_rows) const;

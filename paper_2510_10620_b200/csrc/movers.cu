@@ -28,13 +28,27 @@ __global__ void row_copy_kernel(const RowCopyJob* __restrict__ jobs, const int32
   const bool vec = ((reinterpret_cast<uintptr_t>(J.src) | reinterpret_cast<uintptr_t>(J.dst) |
                      (uintptr_t)J.src_stride | (uintptr_t)J.dst_stride | (uintptr_t)J.row_bytes) & 15) == 0;
   if (vec) {
+    // all of a thread's loads are issued before its stores, so a CTA keeps its whole
+    // chunk (up to 16 KiB) in flight: peer reads over NVLink are latency-bound otherwise
+    constexpr int U = 4;
     const int per_row = J.row_bytes >> 4;
     const int total = (r1 - r0) * per_row;
-    for (int i = threadIdx.x; i < total; i += blockDim.x) {
-      const int r = r0 + i / per_row, c = i % per_row;
-      const uint4* s = reinterpret_cast<const uint4*>(J.src + (int64_t)r * J.src_stride) + c;
-      uint4* d = reinterpret_cast<uint4*>(J.dst + (int64_t)r * J.dst_stride) + c;
-      *d = *s;
+    for (int base = 0; base < total; base += U * blockDim.x) {
+      uint4 v[U];
+      uint4* d[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int i = base + u * blockDim.x + threadIdx.x;
+        d[u] = nullptr;
+        if (i < total) {
+          const int r = r0 + i / per_row, c = i % per_row;
+          v[u] = __ldcs(reinterpret_cast<const uint4*>(J.src + (int64_t)r * J.src_stride) + c);
+          d[u] = reinterpret_cast<uint4*>(J.dst + (int64_t)r * J.dst_stride) + c;
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (d[u]) *d[u] = v[u];
     }
   } else {
     const int per_row = J.row_bytes >> 2;

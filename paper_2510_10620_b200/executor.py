@@ -29,7 +29,8 @@ STATUS = {0: "OK", 1: "Error", 2: "DeadlockError", 3: "TagMismatchError", 4: "Bu
 # Every symbol include/dcpx.h declares (checked by tests/test_capi_symbols.py).
 EXPORTS = ["dcpx_create", "dcpx_create_rank", "dcpx_nccl_unique_id", "dcpx_prepare",
            "dcpx_load_inputs", "dcpx_load_inputs_host", "dcpx_forward", "dcpx_forward_host",
-           "dcpx_backward", "dcpx_backward_host", "dcpx_synchronize", "dcpx_debug_arena",
+           "dcpx_backward", "dcpx_backward_host", "dcpx_load_inputs_dev", "dcpx_forward_dev",
+           "dcpx_backward_dev", "dcpx_synchronize", "dcpx_debug_arena",
            "dcpx_set_option", "dcpx_trace", "dcpx_last_error", "dcpx_version", "dcpx_destroy"]
 
 
@@ -54,6 +55,7 @@ def lib():
         for name in ("dcpx_create", "dcpx_create_rank", "dcpx_nccl_unique_id", "dcpx_prepare",
                      "dcpx_load_inputs", "dcpx_load_inputs_host", "dcpx_forward",
                      "dcpx_forward_host", "dcpx_backward", "dcpx_backward_host",
+                     "dcpx_load_inputs_dev", "dcpx_forward_dev", "dcpx_backward_dev",
                      "dcpx_synchronize", "dcpx_debug_arena", "dcpx_set_option"):
             getattr(L, name).restype = C.c_int
         L.dcpx_create.argtypes = [C.c_int, C.POINTER(C.c_int), C.c_int, C.POINTER(C.c_void_p)]
@@ -66,6 +68,9 @@ def lib():
         L.dcpx_backward.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                     C.c_void_p]
         L.dcpx_backward_host.argtypes = L.dcpx_backward.argtypes
+        L.dcpx_load_inputs_dev.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+        L.dcpx_forward_dev.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+        L.dcpx_backward_dev.argtypes = L.dcpx_backward.argtypes
         L.dcpx_synchronize.argtypes = [C.c_void_p]
         L.dcpx_debug_arena.argtypes = [C.c_void_p, C.c_int, C.c_int, C.POINTER(C.c_void_p),
                                        C.POINTER(C.c_int64)]
@@ -90,6 +95,13 @@ def _report_dict(r: P.c_report) -> dict:
 
 def _ptr(t) -> Optional[int]:
     return None if t is None else t.data_ptr()
+
+
+def _ptrs(ts):
+    """void* array (one entry per plan device) for the dcpx_*_dev calls; None -> NULL."""
+    if ts is None:
+        return None
+    return (C.c_void_p * len(ts))(*[None if t is None else t.data_ptr() for t in ts])
 
 
 class DCPExecutor:
@@ -138,20 +150,31 @@ class DCPExecutor:
         self.bundle = bundle
         self._keep = (keep, g, m, pv)
 
+    # Tensors, or lists with one tensor per plan device in that device's own memory
+    # (the distributed layout: dcpx_*_dev; device d touches only the rows it owns).
     def load_inputs(self, q, k, v):
-        if q.is_cuda:
+        if isinstance(q, (list, tuple)):
+            self._check(lib().dcpx_load_inputs_dev(self._h, _ptrs(q), _ptrs(k), _ptrs(v)))
+        elif q.is_cuda:
             self._check(lib().dcpx_load_inputs(self._h, _ptr(q), _ptr(k), _ptr(v)))
         else:
             self._check(lib().dcpx_load_inputs_host(self._h, _ptr(q), _ptr(k), _ptr(v)))
 
     def forward(self, o=None, lse=None, host: bool = False) -> dict:
         rep = P.c_report()
+        if isinstance(o, (list, tuple)) or isinstance(lse, (list, tuple)):
+            self._check(lib().dcpx_forward_dev(self._h, _ptrs(o), _ptrs(lse), C.byref(rep)))
+            return _report_dict(rep)
         fn = lib().dcpx_forward_host if host else lib().dcpx_forward
         self._check(fn(self._h, _ptr(o), _ptr(lse), C.byref(rep)))
         return _report_dict(rep)
 
     def backward(self, d_o, dq, dk, dv, host: bool = False) -> dict:
         rep = P.c_report()
+        if isinstance(d_o, (list, tuple)):
+            self._check(lib().dcpx_backward_dev(self._h, _ptrs(d_o), _ptrs(dq), _ptrs(dk), _ptrs(dv),
+                                                C.byref(rep)))
+            return _report_dict(rep)
         fn = lib().dcpx_backward_host if host else lib().dcpx_backward
         self._check(fn(self._h, _ptr(d_o), _ptr(dq), _ptr(dk), _ptr(dv), C.byref(rep)))
         return _report_dict(rep)
@@ -165,7 +188,7 @@ class DCPExecutor:
         n = lib().dcpx_trace(self._h, None, 0)
         buf = np.zeros((max(n, 1), 7))
         lib().dcpx_trace(self._h, buf.ctypes.data, n)
-        kinds = ["attn", "merge", "copy", "launch", "wait", "nop"]
+        kinds = ["attn", "merge", "copy", "launch", "wait", "nop", "xfer"]
         return [dict(dev=int(r[0]), instr=int(r[1]), kind=kinds[int(r[2])], division=int(r[3]),
                      pass_="bwd" if r[4] else "fwd", start=r[5], end=r[6]) for r in buf[:n]]
 

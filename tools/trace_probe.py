@@ -29,16 +29,23 @@ def main():
     for _ in range(2):
         ex.load_inputs(q, k, v); ex.forward(o, lse); ex.backward(q, dq, dk, dv)
     ex.set_option("trace", 1)
+
+    def sync():  # align the devices' time origins (each span is relative to its device's t0)
+        for d in range(ng):
+            torch.cuda.synchronize(d)
     ex.load_inputs(q, k, v)
+    sync()
     rf = ex.forward(o, lse)
     tf = ex.trace()
+    sync()
     rb = ex.backward(q, dq, dk, dv)
     tb = ex.trace()
     print(f"{name} on {ng} GPUs: fwd {rf['device_ms']:.3f} ms, bwd {rb['device_ms']:.3f} ms")
     for label, tr in (("fwd", tf), ("bwd", tb)):
         for d in range(b.R):
             rows = [t for t in tr if t["dev"] == d]
-            s = "  ".join(f"{t['kind']}{t['division']}[{t['start']:.2f}-{t['end']:.2f}]" for t in rows)
+            s = "  ".join(f"{t['kind']}{t['division']}[{t['start']:.2f}-{t['end']:.2f}]" if t['kind'] != 'launch'
+                          else f"L{t['division']}@{t['start']:.2f}" for t in rows)
             print(f"{label} dev{d}: {s}")
     for d in range(b.R):
         print(f"dev{d} flops {int(b.dev_flops[d]) / 1e12:.3f} T")
