@@ -321,4 +321,20 @@ __device__ __forceinline__ float fast_exp2(float x) {
   return y;
 }
 
+// 2^x on the FMA / ALU pipes, for x <= 0 (softmax exponents), to take load off MUFU:
+// x = j + f with j = rint(x) (magic-number rounding) and f in [-0.5, 0.5]; 2^f by a cubic
+// fitted to relative error (max 7.5e-5, unbiased; bf16 P has a 3.9e-3 step); j is added
+// straight into the exponent field. x <= -126 (including -inf) gives exactly 0, like
+// ex2.approx.ftz, so fully masked rows keep l = 0.
+__device__ __forceinline__ float soft_exp2(float x) {
+  const float t = fmaxf(x, -127.f);
+  const float jr = t + 12582912.f;  // 1.5 * 2^23: the low mantissa bits hold rint(t)
+  const float f = t - (jr - 12582912.f);
+  float p = fmaf(0.05515746f, f, 0.24261002f);
+  p = fmaf(p, f, 0.6932636f);
+  p = fmaf(p, f, 0.99992824f);
+  const int bits = __float_as_int(p) + (__float_as_int(jr) << 23);
+  return x > -126.f ? __int_as_float(bits) : 0.f;
+}
+
 }  // namespace dcpx

@@ -38,7 +38,8 @@ def build_dcpx(force=False):
     deps = srcs + glob.glob(os.path.join(csrc, "*.h")) + glob.glob(os.path.join(csrc, "*.cuh")) + \
         [os.path.join(REPO, "include", "dcpx.h")]
     # instrumented variants build into build/<variant>/ (never over the product library)
-    variant = "debug" if os.environ.get("DCPX_DEBUG") else "prof" if os.environ.get("DCPX_PROFILE") else ""
+    variant = "debug" if os.environ.get("DCPX_DEBUG") else "prof" if os.environ.get("DCPX_PROFILE") else \
+        os.environ.get("DCPX_VARIANT", "")  # DCPX_VARIANT=name DCPX_DEFS="-DX=1 ..." for experiments
     out = os.path.join(REPO, "build", variant, "libdcpx.so") if variant else \
         os.path.join(REPO, "paper_2510_10620_b200", "libdcpx.so")
     if not force and not _stale(out, deps):
@@ -53,6 +54,8 @@ def build_dcpx(force=False):
             extra = ["-DDCPX_WATCHDOG_REPORT"] if os.environ.get("DCPX_DEBUG") else []
             if os.environ.get("DCPX_PROFILE"):  # per-role wait-cycle counters printed by CTA 0
                 extra.append("-DDCPX_BWD_PROFILE")
+            if os.environ.get("DCPX_VARIANT"):
+                extra += os.environ.get("DCPX_DEFS", "").split()
             _run([NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
                   "-Xptxas", "-warn-spills", *extra, "-c", s, "-o", o])
         objs.append(o)

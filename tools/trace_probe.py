@@ -26,6 +26,12 @@ def main():
     o = torch.empty_like(q)
     lse = torch.empty((H, T), device="cuda")
     dq, dk, dv = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
+    if ng > 1:  # distributed layout, as bench.py: per-device packed buffers
+        devs = [d % ng for d in range(b.R)]
+        rep = lambda x, like=False: [torch.empty_like(x, device=f"cuda:{d}") if like else x.to(f"cuda:{d}")  # noqa: E731
+                                     for d in devs]
+        q, k, v = rep(q), rep(k), rep(v)
+        o, lse, dq, dk, dv = rep(o, True), rep(lse, True), rep(dq, True), rep(dk, True), rep(dv, True)
     for _ in range(2):
         ex.load_inputs(q, k, v); ex.forward(o, lse); ex.backward(q, dq, dk, dv)
     ex.set_option("trace", 1)
