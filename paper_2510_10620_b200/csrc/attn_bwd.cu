@@ -460,8 +460,10 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 #pragma unroll 1
       for (int c = 0; c < 8; ++c) {
         uint32_t r[32];
+        BWD_MARK(t_ld);
         tmem_ld32(lane_addr + 256 + 32 * c, r);
         tmem_wait_ld();
+        BWD_ADD(1, t_ld);
         if (c == 7) {
           tc_fence_before();
           mbar_arrive(&bars.acc_empty);
@@ -470,19 +472,19 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         // wait for everything, including the last step's dQ which used both halves)
         if (wq == 0) {
           if (elect_one()) {
-            if (c == 0) bulk_wait_read<0>();
-            else bulk_wait_read<1>();
+            if (c == 0) BWD_TIMED(5, bulk_wait_read<0>());
+            else BWD_TIMED(5, bulk_wait_read<1>());
           }
           __syncwarp();
         }
-        named_bar_sync(2, 128);
+        BWD_TIMED(2, named_bar_sync(2, 128));
         uint8_t* row = sEpi + (c & 1) * 16384 + j * 128;
 #pragma unroll
         for (int q4 = 0; q4 < 8; ++q4)
           *reinterpret_cast<uint4*>(row + ((q4 ^ (j & 7)) << 4)) =
               make_uint4(r[4 * q4], r[4 * q4 + 1], r[4 * q4 + 2], r[4 * q4 + 3]);
-        fence_proxy_async_smem();
-        named_bar_sync(2, 128);
+        BWD_TIMED(3, fence_proxy_async_smem());
+        BWD_TIMED(3, named_bar_sync(2, 128));
         if (wq == 0) {
           if (elect_one()) {
             tma_reduce_add_2d(&tm_dkv, sEpi + (c & 1) * 16384, 32 * (c & 3),
@@ -498,7 +500,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       if (elect_one()) bulk_wait<0>();
       __syncwarp();
     }
-    if (wq == 0 && lane == 0) BWD_PROF_PRINT("drain", "dq_full", "bar", "tma_read", "acc_full", "epilogue", "-");
+    if (wq == 0 && lane == 0) BWD_PROF_PRINT("drain", "dq_full", "bar+ep_ld", "ep_bar1", "ep_fence+bar2", "epilogue", "epi_wait");
   }
   tc_fence_before();
   __syncthreads();
