@@ -135,6 +135,7 @@ def main():
     ap.add_argument("--config", default="cfg2")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -265,8 +266,8 @@ def main():
     # algorithmic FLOPs of all launches / GPU-time summed over the devices' launches
     pk, src = peaks()
     peak = pk.get("bf16_tflops_sustained", pk["bf16_tflops"])
-    bwd_kernel_ms = sum(bwd_k) / len(bwd_k)
-    fwd_kernel_ms = sum(fwd_k) / len(fwd_k)
+    bwd_kernel_ms = sum(bwd_k) / len(bwd_k) or 1e-9
+    fwd_kernel_ms = sum(fwd_k) / len(fwd_k) or 1e-9
     bwd_flops, fwd_flops = 2.5 * F_fwd, F_fwd
     dominant = "attn_bwd_kernel" if bwd_kernel_ms >= fwd_kernel_ms else "attn_fwd_kernel"
     if dominant == "attn_bwd_kernel":
