@@ -42,9 +42,25 @@ struct DeviceGuard {
   int prev = 0;
   explicit DeviceGuard(int d) {
     cudaGetDevice(&prev);
-    cudaSetDevice(d);
+    if (prev != d) cudaSetDevice(d);
   }
   ~DeviceGuard() { cudaSetDevice(prev); }
+};
+
+// Current-device cursor for the enqueue loops: switches only when the device changes and
+// restores the caller's device at the end (the loops visit thousands of ops per call).
+struct DeviceCursor {
+  int saved = 0, cur = -1;
+  DeviceCursor() { cudaGetDevice(&saved); cur = saved; }
+  void to(int d) {
+    if (d != cur) {
+      cudaSetDevice(d);
+      cur = d;
+    }
+  }
+  ~DeviceCursor() {
+    if (cur != saved) cudaSetDevice(saved);
+  }
 };
 
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
@@ -551,6 +567,21 @@ void Executor::prepare(int nplans, const dcpx_plan_view* plans, const dcpx_graph
   for (int d = 0; d < R_; ++d) {
     DeviceGuard g(dev_[d].ordinal);
     CUDA_OK(cudaDeviceSynchronize());
+  }
+  // enqueue orders per pass without the ops that launch nothing (fused reductions, remapped
+  // copies; the backward also skips the output stage and the forward-only merges / copies)
+  fwd_live_.clear();
+  bwd_live_.clear();
+  {
+    const int T = R_ ? plans_[0].divisions : 0;
+    for (const auto& [d, i] : order_) {
+      const Op& op = dev_[d].prog[i];
+      if (op.kind == OpKind::kNop) continue;
+      fwd_live_.push_back({d, i});
+      if (plans_[d].ins[i].division < T &&
+          (op.kind == OpKind::kFwdAttn || op.kind == OpKind::kCommLaunch || op.kind == OpKind::kCommWait))
+        bwd_live_.push_back({d, i});
+    }
   }
   prepared_ = true;
 }
@@ -1348,10 +1379,11 @@ void Executor::forward(void* const* o_out, float* const* lse_out, dcpx_report* r
     CUDA_OK(cudaEventRecord(ready_ev[d], dev_[d].cs));
   }
   trace_begin();
-  for (const auto& [d, i] : order_) {
+  DeviceCursor cursor;
+  for (const auto& [d, i] : fwd_live_) {
     DevState& D = dev_[d];
     Op& op = D.prog[i];
-    DeviceGuard gd(D.ordinal);
+    cursor.to(D.ordinal);
     TraceScope ts(this, d, static_cast<int>(i), op.kind == OpKind::kCommWait ? D.ms : D.cs, 0, op);
     switch (op.kind) {
       case OpKind::kFwdAttn: {
@@ -1588,11 +1620,11 @@ void Executor::backward(const void* const* d_o, void* const* dq, void* const* dk
     CUDA_OK(cudaEventRecord(ready_ev[d], dev_[d].cs));
   }
   trace_begin();
-  for (const auto& [d, i] : order_) {
+  DeviceCursor cursor;
+  for (const auto& [d, i] : bwd_live_) {  // the output stage has no backward counterpart
     DevState& D = dev_[d];
     Op& op = D.prog[i];
-    if (plans_[d].ins[i].division >= T) continue;  // output stage has no backward counterpart
-    DeviceGuard gd(D.ordinal);
+    cursor.to(D.ordinal);
     TraceScope ts(this, d, static_cast<int>(i), op.kind == OpKind::kCommWait ? D.ms : D.cs, 1, op);
     switch (op.kind) {
       case OpKind::kFwdAttn: {

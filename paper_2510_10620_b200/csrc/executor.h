@@ -200,6 +200,7 @@ class Executor {
   std::vector<DevState> dev_;
   // global issue order from the lockstep simulation: (device, op index)
   std::vector<std::pair<int, int>> order_;
+  std::vector<std::pair<int, int>> fwd_live_, bwd_live_;  // order_ without ops that launch nothing
   std::vector<void*> allocs_;  // (ordinal, ptr) freed in destructor
   std::vector<int> alloc_dev_;
   uint32_t* diag_ = nullptr;   // host-mapped watchdog report buffer (see sm100.cuh)

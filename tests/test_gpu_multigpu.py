@@ -51,7 +51,7 @@ def test_multi_gpu_forward_backward(R):
 def test_per_device_io_matches_single_buffer(R):
     """dcpx_*_dev (distributed layout): device d reads its resident rows from its own
     buffer and writes only the rows it owns; the union of the per-device outputs equals
-    the single-buffer call's output bit for bit. Runs on 1 GPU (plan devices emulated)
+    the single-buffer call's output (O, LSE bit for bit; gradients to bf16 rounding). Runs on 1 GPU (plan devices emulated)
     or spreads the plan devices over the GPUs present."""
     import torch
 
@@ -87,6 +87,12 @@ def test_per_device_io_matches_single_buffer(R):
     ex.synchronize()
     for key, ref in (("o", o), ("lse", lse), ("dq", dq), ("dk", dk), ("dv", dv)):
         parts = [p[key].float().cpu() for p in per]
-        # owned rows are disjoint: exactly one device wrote each row
-        assert torch.equal(sum(parts), ref.float().cpu()), key
+        # owned rows are disjoint: exactly one device wrote each row. O and LSE are
+        # deterministic; gradients accumulate through atomic reduce-adds (order varies
+        # between runs), so they agree to bf16 rounding rather than bit for bit.
+        got, want = sum(parts), ref.float().cpu()
+        if key in ("o", "lse"):
+            assert torch.equal(got, want), key
+        else:
+            assert rel_err(got.numpy(), want.numpy()) <= 4e-3, key
     ex.close()
