@@ -133,6 +133,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="dcpx", choices=["dcpx", "reference"])
     ap.add_argument("--config", default="cfg2")
+    ap.add_argument("--placement", default="dcp", choices=["dcp", "ring", "zigzag"],
+                    help="plan placement: DCP (default) or the paper's baselines (cfg2 only)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
 
@@ -150,12 +152,13 @@ def main():
         if dist is not None:
             dist.barrier()
 
-    name = f"{args.config}_R{N}"
+    name = f"{args.config}_R{N}" if args.placement == "dcp" else f"{args.config}_{args.placement}_R{N}"
     metric = "masked attention fwd+bwd TFLOPS"
     config = {"workload": f"{args.config}: 8B-GPT attention layer (32 q / 8 kv heads, d 128), causal, "
                           "LongAlign-skewed 64K-token batch (6 seqs, 63,855 tokens), block 1024, T 4, "
                           f"DCP plan for {N} device(s)", "global_batch_tokens": None, "heads": "32/8",
-              "block": 1024, "parallelism": f"dcp{N}", "l2": "inputs larger than L2 (q alone 523 MB)"}
+              "block": 1024, "parallelism": f"{args.placement}{N}", "placement": args.placement,
+              "l2": "inputs larger than L2 (q alone 523 MB)"}
 
     if args.impl == "reference":
         if rank != 0:

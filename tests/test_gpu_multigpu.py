@@ -96,3 +96,31 @@ def test_per_device_io_matches_single_buffer(R):
         else:
             assert rel_err(got.numpy(), want.numpy()) <= 4e-3, key
     ex.close()
+
+
+@pytest.mark.parametrize("placement", ["ring", "zigzag"])
+def test_baseline_placements_on_gpu(placement):
+    """the paper's baseline placements (inc/baselines.hpp:46-112) planned by
+    the reference and executed unchanged by the same GPU executor; plan devices spread
+    over the GPUs present (emulated on one GPU if there is only one)."""
+    import torch
+
+    import oracle as O
+    from paper_2510_10620_b200.executor import DCPExecutor
+    R = 4
+    bundle = bundle_for(MIXED_SPECS, H=4, G=2, block=256, R=R, placement=placement)
+    (q, k, v), (q64, k64, v64) = inputs(bundle, seed=11)
+    T = bundle.total_tokens
+    ex = DCPExecutor([d % _ngpu() for d in range(R)])
+    ex.prepare(bundle)
+    o = torch.zeros((T, 4, 128), dtype=torch.bfloat16, device="cuda:0")
+    lse = torch.zeros((4, T), device="cuda:0")
+    ex.load_inputs(q.cuda(), k.cuda(), v.cuda())
+    rep = ex.forward(o, lse)
+    ex.synchronize()
+    o_ref, lse_ref, orep, st, msg = O.run(bundle, q64, k64, v64)
+    assert st == 0, msg
+    assert rel_err(o.float().cpu().numpy(), o_ref) <= O_TOL
+    assert lse_err(lse.cpu().numpy(), lse_ref) <= LSE_TOL
+    assert rep["total_bytes"] == orep.total_bytes == int(bundle.volume[0])
+    ex.close()

@@ -43,6 +43,11 @@ CONFIGS = {
     "cfg2_R2": (synth("causal", 65536, 65536, 2), 2, 1024, {}),
     "cfg2_R4": (synth("causal", 65536, 65536, 2), 4, 1024, {}),
     "cfg2_R8": (synth("causal", 65536, 65536, 2), 8, 1024, {}),
+    # the paper's baseline placements of the same batch (inc/baselines.hpp:46-112)
+    "cfg2_ring_R4": (synth("causal", 65536, 65536, 2), 4, 1024, {"placement": "ring"}),
+    "cfg2_ring_R8": (synth("causal", 65536, 65536, 2), 8, 1024, {"placement": "ring"}),
+    "cfg2_zigzag_R4": (synth("causal", 65536, 65536, 2), 4, 1024, {"placement": "zigzag"}),
+    "cfg2_zigzag_R8": (synth("causal", 65536, 65536, 2), 8, 1024, {"placement": "zigzag"}),
     # configs[2]: 128K lambda (sink 64 + window 4096), 1/2/4/8 GPUs
     "cfg3_R1": (synth("lambda", 131072, 131072, 0), 1, 1024, {}),
     "cfg3_R2": (synth("lambda", 131072, 131072, 0), 2, 1024, {}),
