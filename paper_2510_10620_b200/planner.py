@@ -206,8 +206,10 @@ def plan(batch: Batch, devices: int, block_size: int, divisions: int = 4,
          eps_inter: float = 0.4, eps_intra: float = 0.1, eps_data: float = 0.05, seed: int = 0,
          machines: int = 1, placement: str = "dcp", group_dev: Optional[np.ndarray] = None,
          comp_dev: Optional[np.ndarray] = None, verify: bool = True,
-         max_slots_per_kind: int = 0) -> P.PlanBundle:
-    """Runs the reference planner (plan_batch, pipeline.hpp:29-38) and flattens it."""
+         max_slots_per_kind: int = 0, json_dir: Optional[str] = None) -> P.PlanBundle:
+    """Runs the reference planner (plan_batch, pipeline.hpp:29-38) and flattens it.
+    json_dir: also write the plan in the reference's file formats there (batch.jsonl,
+    graph.json, placement.json, plan_d<d>.json, with the reference's own writers)."""
     cfg = CfgC()
     cfg.machines, cfg.devices_per_machine = machines, devices // machines
     cfg.divisions, cfg.max_slots_per_kind, cfg.block_size = divisions, max_slots_per_kind, block_size
@@ -220,6 +222,8 @@ def plan(batch: Batch, devices: int, block_size: int, divisions: int = 4,
     _check(lib().dcpp_plan(batch._h, C.byref(cfg), mode, gd.ctypes.data if gd is not None else None,
                            cd.ctypes.data if cd is not None else None, C.byref(h)))
     try:
+        if json_dir is not None:
+            _check(lib().dcpp_dump_json(h, batch._h, json_dir.encode()))
         hdr = _arr(h, "header", 0, np.int32)
         R, T, H, G, D, bpe = (int(x) for x in hdr[:6])
         devs = []

@@ -25,6 +25,11 @@
 
 #include "dcp/baselines.hpp"
 #include "dcp/pipeline.hpp"
+#if __has_include(<json.hpp>)
+#include <filesystem>
+#include "dcp/io.hpp"  // the reference's plan / graph / placement JSON writers (io.hpp:72-352)
+#define DCPP_HAVE_JSON 1
+#endif
 #include "dcp/synth.hpp"
 #include "fixtures.hpp"
 #include "../include/dcpx.h"
@@ -437,6 +442,44 @@ int dcpp_array(dcpp_planned* p, const char* name, int device, const void** ptr, 
 #undef RET
   g_err = "dcpp_array: unknown array " + n;
   return DCPX_ERROR;
+}
+
+// Writes the planned batch in the reference's own file formats, with the reference's own
+// writers: batch.jsonl (write_sequences_jsonl, io.hpp:72-88), graph.json
+// (block_graph_to_json, :135-174), placement.json (placement_to_json, :183-216) and
+// plan_d<d>.json (plan_to_json, :271-350). DCPX_UNSUPPORTED when built without json.hpp.
+int dcpp_dump_json(const dcpp_planned* p, const dcpp_batch* b, const char* dir) {
+#ifdef DCPP_HAVE_JSON
+  try {
+    namespace fs = std::filesystem;
+    fs::create_directories(dir);
+    const fs::path d(dir);
+    dcp::BatchHeader h;
+    h.heads = b->batch.heads;
+    h.kv_groups = b->batch.kv_groups;
+    h.head_dim = b->batch.head_dim;
+    h.token_budget = b->batch.token_budget;
+    h.bytes_per_element = b->batch.bytes_per_element;
+    std::ostringstream os;
+    dcp::write_sequences_jsonl(os, h, b->batch.sequences);
+    dcp::write_file((d / "batch.jsonl").string(), os.str());
+    dcp::write_file((d / "graph.json").string(), dcp::block_graph_to_json(p->pb.graph).dump(1));
+    dcp::write_file((d / "placement.json").string(),
+                    dcp::placement_to_json(p->pb.graph, p->pb.placement).dump(1));
+    for (size_t i = 0; i < p->pb.plans.size(); ++i)
+      dcp::write_file((d / ("plan_d" + std::to_string(i) + ".json")).string(),
+                      dcp::plan_to_json(p->pb.plans[i]).dump(1));
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
+#else
+  (void)p;
+  (void)b;
+  (void)dir;
+  g_err = "dcpp_dump_json: planner shim built without json.hpp";
+  return DCPX_UNSUPPORTED;
+#endif
 }
 
 }  // extern "C"

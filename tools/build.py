@@ -63,6 +63,12 @@ def build_dcpx(force=False):
     return out
 
 
+# nlohmann json (the reference's io.hpp dependency, absent from the reference tree): the
+# copy vendored by cudnn_frontend in this image, used only for the plan-file writer.
+NLOHMANN = os.path.join(sys.prefix, "lib", f"python{sys.version_info.major}.{sys.version_info.minor}",
+                        "site-packages", "include", "cudnn_frontend", "thirdparty", "nlohmann")
+
+
 def build_planner(force=False):
     src = os.path.join(REPO, "planner", "dcp_planner_capi.cpp")
     out = os.path.join(REPO, "planner", "_build", "libdcpplanner.so")
@@ -72,7 +78,8 @@ def build_planner(force=False):
         return out
     if force or _stale(out, [src, os.path.join(REPO, "include", "dcpx.h")]):
         os.makedirs(os.path.dirname(out), exist_ok=True)
-        _run(["g++", "-std=c++20", "-O3", "-fPIC", "-shared", f"-I{REF}/include", f"-I{REF}/tests",
+        nl = [f"-I{NLOHMANN}"] if os.path.exists(os.path.join(NLOHMANN, "json.hpp")) else []
+        _run(["g++", "-std=c++20", "-O3", "-fPIC", "-shared", f"-I{REF}/include", f"-I{REF}/tests", *nl,
               src, "-o", out, "-pthread"])
     return out
 
