@@ -16,6 +16,17 @@ def test_dropin_reference_suite():
     assert r.returncode == 0 and "DROPIN PASS" in r.stdout, r.stdout + r.stderr
 
 
+def test_lookahead_pipeline_with_gpu_consumer():
+    """SURVEY 8(f)2: dcp::gpu::pipeline_run (include/dcp_gpu_pipeline.hpp) vs the
+    reference's pipeline_run (pipeline.hpp:105) on the same batches: identical reports,
+    look-ahead protocol respected (tests/cpp/test_gpu_pipeline.cpp)."""
+    binp = os.path.join(os.path.dirname(BIN), "test_gpu_pipeline")
+    assert os.path.exists(binp), "pipeline test binary not built (tools/build.py)"
+    r = subprocess.run([binp], capture_output=True, text=True, timeout=900)
+    print(r.stdout)
+    assert r.returncode == 0 and "OK (0 failures)" in r.stdout, r.stdout + r.stderr
+
+
 def test_plan_from_reference_json_files_on_gpu():
     """a plan read from the reference's own plan files (planio) runs on the
     GPU exactly like the same plan coming from the planner shim."""

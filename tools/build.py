@@ -93,12 +93,24 @@ def build_oracle(force=False):
 
 def build_dropin_test(force=False):
     """tests/cpp/test_dcp_gpu_run: the reference's executor tests with dcp::gpu::run swapped in
-    (include/dcp_gpu.hpp), compiled against the unchanged reference headers."""
-    src = os.path.join(REPO, "tests", "cpp", "test_dcp_gpu_run.cpp")
-    out = os.path.join(REPO, "tests", "cpp", "_build", "test_dcp_gpu_run")
+    (include/dcp_gpu.hpp), and tests/cpp/test_gpu_pipeline: the look-ahead pipeline with the
+    GPU executor as consumer (include/dcp_gpu_pipeline.hpp) against the reference's
+    pipeline_run; both compiled against the unchanged reference headers."""
     lib = os.path.join(REPO, "paper_2510_10620_b200", "libdcpx.so")
-    if not os.path.isdir(os.path.join(REF, "include", "dcp")):
-        return out
+    out = None
+    for name, hdr in (("test_dcp_gpu_run", "dcp_gpu.hpp"), ("test_gpu_pipeline", "dcp_gpu_pipeline.hpp")):
+        src = os.path.join(REPO, "tests", "cpp", name + ".cpp")
+        out = os.path.join(REPO, "tests", "cpp", "_build", name)
+        if not os.path.isdir(os.path.join(REF, "include", "dcp")):
+            continue
+        deps = [src, lib, os.path.join(REPO, "include", "dcp_gpu.hpp"), os.path.join(REPO, "include", hdr),
+                os.path.join(REPO, "include", "dcpx.h")]
+        if force or _stale(out, deps):
+            os.makedirs(os.path.dirname(out), exist_ok=True)
+            _run(["g++", "-std=c++20", "-O2", f"-I{REF}/include", f"-I{REF}/tests", f"-I{REPO}/include",
+                  "-I/usr/local/cuda/include", src, "-o", out, lib, "-L/usr/local/cuda/lib64", "-lcudart",
+                  "-Wl,-rpath,$ORIGIN/../../../paper_2510_10620_b200", "-pthread"])
+    return out
     deps = [src, lib, os.path.join(REPO, "include", "dcp_gpu.hpp"), os.path.join(REPO, "include", "dcpx.h")]
     if force or _stale(out, deps):
         os.makedirs(os.path.dirname(out), exist_ok=True)
