@@ -187,7 +187,9 @@ dcpx_status dcpx_prepare(dcpx_ctx* ctx, int nplans, const dcpx_plan_view* plans,
  * buffer (peer-to-peer when it lives on another GPU; see dcpx_load_inputs_dev for the
  * distributed layout). Scatters rows into the resident slots. */
 dcpx_status dcpx_load_inputs(dcpx_ctx* ctx, const void* q, const void* k, const void* v);
-/* Same with host (pinned or pageable) pointers; host->device copies are inside. */
+/* Same with host (pinned or pageable) pointers; host->device copies are inside.
+ * Asynchronous: returns once the upload is enqueued (double-buffered device staging);
+ * the host buffers must stay unchanged until the following dcpx_synchronize. */
 dcpx_status dcpx_load_inputs_host(dcpx_ctx* ctx, const void* q, const void* k, const void* v);
 
 /* Executes the plan forward. o_out [T][H][D] bf16 and lse_out [H][T] fp32 (may be
@@ -199,6 +201,10 @@ dcpx_status dcpx_forward_host(dcpx_ctx* ctx, void* o_out, float* lse_out, dcpx_r
  * dk, dv [T][G][D] bf16 out (owned rows). */
 dcpx_status dcpx_backward(dcpx_ctx* ctx, const void* d_o, void* dq, void* dk, void* dv,
                           dcpx_report* rep);
+/* Host-buffer backward, asynchronous like dcpx_load_inputs_host: dq/dk/dv are valid after
+ * the next dcpx_synchronize (uploads and downloads run on their own streams, so
+ * consecutive steps overlap their PCIe traffic with compute). dcpx_forward_host is
+ * synchronous (o_out/lse_out valid on return). */
 dcpx_status dcpx_backward_host(dcpx_ctx* ctx, const void* d_o, void* dq, void* dk, void* dv,
                                dcpx_report* rep);
 

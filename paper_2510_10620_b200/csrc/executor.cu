@@ -155,6 +155,20 @@ Executor::Executor(int ndev, const int* ordinals) : R_(ndev) {
     CUDA_OK(cudaEventCreate(&dev_[d].t0));
     CUDA_OK(cudaEventCreate(&dev_[d].t1));
   }
+  if (R_ > 0) {
+    DeviceGuard g(ordinals_[0]);
+    CUDA_OK(cudaStreamCreateWithFlags(&h2d_, cudaStreamNonBlocking));
+    CUDA_OK(cudaStreamCreateWithFlags(&d2h_, cudaStreamNonBlocking));
+  }
+}
+
+cudaEvent_t Executor::staging_event(int d) {
+  DeviceGuard g(dev_[d].ordinal);
+  cudaEvent_t e;
+  CUDA_OK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  staging_events_.push_back(e);
+  staging_event_dev_.push_back(dev_[d].ordinal);
+  return e;
 }
 
 Executor::~Executor() {
@@ -162,6 +176,15 @@ Executor::~Executor() {
     DeviceGuard g(d.ordinal);
     if (d.cs) cudaStreamSynchronize(d.cs);
     if (d.ms) cudaStreamSynchronize(d.ms);
+  }
+  if (R_ > 0) {
+    DeviceGuard g(dev_[0].ordinal);
+    if (h2d_) { cudaStreamSynchronize(h2d_); cudaStreamDestroy(h2d_); }
+    if (d2h_) { cudaStreamSynchronize(d2h_); cudaStreamDestroy(d2h_); }
+  }
+  for (size_t i = 0; i < staging_events_.size(); ++i) {
+    DeviceGuard g(staging_event_dev_[i]);
+    cudaEventDestroy(staging_events_[i]);
   }
   free_all();
   if (diag_) cudaFreeHost(diag_);
@@ -336,8 +359,13 @@ std::pair<cudaEvent_t, cudaEvent_t> Executor::kernel_events(int d) {
 void Executor::prepare(int nplans, const dcpx_plan_view* plans, const dcpx_graph_view* gv,
                        const dcpx_mask_view* mv) {
   if (nplans != R_) throw Failure(DCPX_ERROR, "run: plan count does not match topology");  // simexec.hpp:211
+  synchronize();  // asynchronous host I/O of a previous plan may still be in flight
   free_all();
-  in_stage_ = out_stage_ = bwd_stage_ = nullptr;
+  out_stage_ = nullptr;
+  for (Staging* st : {&in_st_, &bwd_st_})
+    for (int k = 0; k < 2; ++k) {  // (events stay alive in staging_events_ and are reused)
+      st->buf[k] = nullptr;
+    }
   fwd_done_ = false;
   for (auto& d : dev_) {
     d.prog.clear();
@@ -1331,21 +1359,27 @@ void Executor::load_inputs(const void* const* q, const void* const* k, const voi
   if (!prepared_) throw Failure(DCPX_ERROR, "dcpx_load_inputs before dcpx_prepare");
   const int64_t TT = g_.total_tokens();
   std::vector<const void*> sq(q, q + R_), sk(k, k + R_), sv(v, v + R_);
+  int slot = -1;
   if (host) {
-    // stage once on the first device; peers read it over NVLink
+    // upload into staging slot k on the h2d stream once the slot's previous scatters are
+    // done; peers read it over NVLink. The call returns without waiting for the copy.
     DevState& D0 = dev_[0];
     DeviceGuard gd(D0.ordinal);
     const size_t bq = TT * g_.H * 256, bk = TT * g_.G * 256;
-    if (!in_stage_) in_stage_ = static_cast<char*>(alloc(0, bq + 2 * bk));
-    char* buf = in_stage_;
-    CUDA_OK(cudaMemcpyAsync(buf, q[0], bq, cudaMemcpyHostToDevice, D0.cs));
-    CUDA_OK(cudaMemcpyAsync(buf + bq, k[0], bk, cudaMemcpyHostToDevice, D0.cs));
-    CUDA_OK(cudaMemcpyAsync(buf + bq + bk, v[0], bk, cudaMemcpyHostToDevice, D0.cs));
-    cudaEvent_t e = event(0);
-    CUDA_OK(cudaEventRecord(e, D0.cs));
-    for (int d = 1; d < R_; ++d) {
+    slot = in_st_.next;
+    in_st_.next ^= 1;
+    char*& buf = in_st_.buf[slot];
+    if (!buf) buf = static_cast<char*>(alloc(0, bq + 2 * bk));
+    for (cudaEvent_t e : in_st_.free[slot]) CUDA_OK(cudaStreamWaitEvent(h2d_, e, 0));
+    CUDA_OK(cudaMemcpyAsync(buf, q[0], bq, cudaMemcpyHostToDevice, h2d_));
+    CUDA_OK(cudaMemcpyAsync(buf + bq, k[0], bk, cudaMemcpyHostToDevice, h2d_));
+    CUDA_OK(cudaMemcpyAsync(buf + bq + bk, v[0], bk, cudaMemcpyHostToDevice, h2d_));
+    if (!in_st_.up[slot]) in_st_.up[slot] = staging_event(0);
+    cudaEvent_t up = in_st_.up[slot];
+    CUDA_OK(cudaEventRecord(up, h2d_));
+    for (int d = 0; d < R_; ++d) {
       DeviceGuard g2(dev_[d].ordinal);
-      CUDA_OK(cudaStreamWaitEvent(dev_[d].cs, e, 0));
+      CUDA_OK(cudaStreamWaitEvent(dev_[d].cs, up, 0));
     }
     std::fill(sq.begin(), sq.end(), buf);
     std::fill(sk.begin(), sk.end(), buf + bq);
@@ -1358,6 +1392,15 @@ void Executor::load_inputs(const void* const* q, const void* const* k, const voi
     launch_row_copy(D.scatter_k.dj, D.cs, reinterpret_cast<int64_t>(sk[d]), 0);
     launch_row_copy(D.scatter_v.dj, D.cs, reinterpret_cast<int64_t>(sv[d]), 0);
     CUDA_OK(cudaGetLastError());
+  }
+  if (slot >= 0) {  // the slot is free again once every device has scattered from it
+    auto& fr = in_st_.free[slot];
+    if (fr.empty())
+      for (int d = 0; d < R_; ++d) fr.push_back(staging_event(d));
+    for (int d = 0; d < R_; ++d) {
+      DeviceGuard gd(dev_[d].ordinal);
+      CUDA_OK(cudaEventRecord(fr[d], dev_[d].cs));
+    }
   }
 }
 
@@ -1569,21 +1612,29 @@ void Executor::backward(const void* const* d_o, void* const* dq, void* const* dk
     DeviceGuard gd(D.ordinal);
     if (opt.timing) CUDA_OK(cudaEventRecord(D.t0, D.cs));
   }
+  int slot = -1;
   if (host) {
+    // dO up on h2d_ into staging slot k (once the slot's previous downloads are done);
+    // dQ/dK/dV come back through the same slot on d2h_ at the end. Asynchronous.
     DevState& D0 = dev_[0];
     DeviceGuard gd(D0.ordinal);
-    if (!bwd_stage_) bwd_stage_ = static_cast<char*>(alloc(0, 2 * bq + 2 * bk));
-    CUDA_OK(cudaMemcpyAsync(bwd_stage_, d_o[0], bq, cudaMemcpyHostToDevice, D0.cs));
-    cudaEvent_t e = event(0);
-    CUDA_OK(cudaEventRecord(e, D0.cs));
-    for (int d = 1; d < R_; ++d) {
+    slot = bwd_st_.next;
+    bwd_st_.next ^= 1;
+    char*& buf = bwd_st_.buf[slot];
+    if (!buf) buf = static_cast<char*>(alloc(0, 2 * bq + 2 * bk));
+    for (cudaEvent_t e : bwd_st_.free[slot]) CUDA_OK(cudaStreamWaitEvent(h2d_, e, 0));
+    CUDA_OK(cudaMemcpyAsync(buf, d_o[0], bq, cudaMemcpyHostToDevice, h2d_));
+    if (!bwd_st_.up[slot]) bwd_st_.up[slot] = staging_event(0);
+    cudaEvent_t up = bwd_st_.up[slot];
+    CUDA_OK(cudaEventRecord(up, h2d_));
+    for (int d = 0; d < R_; ++d) {
       DeviceGuard g2(dev_[d].ordinal);
-      CUDA_OK(cudaStreamWaitEvent(dev_[d].cs, e, 0));
+      CUDA_OK(cudaStreamWaitEvent(dev_[d].cs, up, 0));
     }
-    std::fill(ddo.begin(), ddo.end(), bwd_stage_);
-    std::fill(ddq.begin(), ddq.end(), ddq[0] ? bwd_stage_ + bq : nullptr);
-    std::fill(ddk.begin(), ddk.end(), ddk[0] ? bwd_stage_ + 2 * bq : nullptr);
-    std::fill(ddv.begin(), ddv.end(), ddv[0] ? bwd_stage_ + 2 * bq + bk : nullptr);
+    std::fill(ddo.begin(), ddo.end(), buf);
+    std::fill(ddq.begin(), ddq.end(), ddq[0] ? buf + bq : nullptr);
+    std::fill(ddk.begin(), ddk.end(), ddk[0] ? buf + 2 * bq : nullptr);
+    std::fill(ddv.begin(), ddv.end(), ddv[0] ? buf + 2 * bq + bk : nullptr);
   }
   const float scale = static_cast<float>(1.0 / std::sqrt(static_cast<double>(g_.D)));
   for (int d = 0; d < R_; ++d) {
@@ -1705,20 +1756,21 @@ void Executor::backward(const void* const* d_o, void* const* dq, void* const* dk
   }
   if (host) {
     DevState& D0 = dev_[0];
-    for (int d = 1; d < R_; ++d) {
+    DeviceGuard gd(D0.ordinal);
+    for (int d = 0; d < R_; ++d) {  // every device's conversions into the slot are done
       cudaEvent_t e = event(d);
       {
         DeviceGuard g2(dev_[d].ordinal);
         CUDA_OK(cudaEventRecord(e, dev_[d].cs));
       }
-      DeviceGuard g3(D0.ordinal);
-      CUDA_OK(cudaStreamWaitEvent(D0.cs, e, 0));
+      CUDA_OK(cudaStreamWaitEvent(d2h_, e, 0));
     }
-    DeviceGuard gd(D0.ordinal);
-    if (ddq[0]) CUDA_OK(cudaMemcpyAsync(dq[0], ddq[0], bq, cudaMemcpyDeviceToHost, D0.cs));
-    if (ddk[0]) CUDA_OK(cudaMemcpyAsync(dk[0], ddk[0], bk, cudaMemcpyDeviceToHost, D0.cs));
-    if (ddv[0]) CUDA_OK(cudaMemcpyAsync(dv[0], ddv[0], bk, cudaMemcpyDeviceToHost, D0.cs));
-    CUDA_OK(cudaStreamSynchronize(D0.cs));
+    if (ddq[0]) CUDA_OK(cudaMemcpyAsync(dq[0], ddq[0], bq, cudaMemcpyDeviceToHost, d2h_));
+    if (ddk[0]) CUDA_OK(cudaMemcpyAsync(dk[0], ddk[0], bk, cudaMemcpyDeviceToHost, d2h_));
+    if (ddv[0]) CUDA_OK(cudaMemcpyAsync(dv[0], ddv[0], bk, cudaMemcpyDeviceToHost, d2h_));
+    auto& fr = bwd_st_.free[slot];
+    if (fr.empty()) fr.push_back(staging_event(0));
+    CUDA_OK(cudaEventRecord(fr[0], d2h_));
   }
   fill_report(rep, true);
 }
@@ -1728,6 +1780,11 @@ void Executor::synchronize() {
     DeviceGuard gd(D.ordinal);
     CUDA_OK(cudaStreamSynchronize(D.cs));
     CUDA_OK(cudaStreamSynchronize(D.ms));
+  }
+  if (R_ > 0) {
+    DeviceGuard gd(dev_[0].ordinal);
+    if (h2d_) CUDA_OK(cudaStreamSynchronize(h2d_));
+    if (d2h_) CUDA_OK(cudaStreamSynchronize(d2h_));
   }
 }
 

@@ -204,9 +204,22 @@ class Executor {
   std::vector<void*> allocs_;  // (ordinal, ptr) freed in destructor
   std::vector<int> alloc_dev_;
   uint32_t* diag_ = nullptr;   // host-mapped watchdog report buffer (see sm100.cuh)
-  char* in_stage_ = nullptr;   // host-input staging on device 0 (load_inputs_host)
-  char* out_stage_ = nullptr;  // host-output staging on device 0 (forward_host)
-  char* bwd_stage_ = nullptr;  // host staging for backward (dO in, dQ/dK/dV out)
+  // Host I/O goes through device-0 staging. load_inputs_host / backward_host are
+  // asynchronous: two staging slots alternate, uploads run on h2d_ and downloads on d2h_
+  // (PCIe is full duplex), so step i+1's uploads and step i's downloads overlap step i's
+  // compute; free[k] holds the events after which slot k may be overwritten.
+  struct Staging {
+    char* buf[2] = {nullptr, nullptr};
+    std::vector<cudaEvent_t> free[2];  // per plan device (backward: entry 0 only)
+    cudaEvent_t up[2] = {nullptr, nullptr};  // upload into slot k finished (h2d_)
+    int next = 0;
+  };
+  Staging in_st_, bwd_st_;
+  char* out_stage_ = nullptr;  // host-output staging on device 0 (forward_host, synchronous)
+  cudaStream_t h2d_ = nullptr, d2h_ = nullptr;  // on device 0
+  cudaEvent_t staging_event(int d);              // persistent (not from the per-call pool)
+  std::vector<cudaEvent_t> staging_events_;
+  std::vector<int> staging_event_dev_;
   bool fwd_done_ = false;
   std::vector<uint64_t> bwd_send_, bwd_recv_;  // planned backward bytes per device
   bool prepared_ = false;
