@@ -480,7 +480,6 @@ void Executor::prepare(int nplans, const dcpx_plan_view* plans, const dcpx_graph
           }
         } else if (I.op == DCPX_OP_REDUCTION) {
           if (I.count < 1) throw Failure(DCPX_ERROR, "exec_reduction: no partials");  // simexec.hpp:81
-          if (I.count > kMaxMergeSrcs) throw Failure(DCPX_UNSUPPORTED, "reduction with more than 64 partials");
           for (int i = 0; i < I.count; ++i) require(2, P.srcs[I.offset + i], "reduction");
           check_slot(2, I.dst);
           written[2].insert(I.dst);

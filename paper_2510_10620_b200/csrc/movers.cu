@@ -72,31 +72,39 @@ __global__ void merge_kernel(const MergeJob* __restrict__ jobs, const int32_t* _
   const int row_in_job = (b - first_chunk[j]) * 16 + (threadIdx.x >> 4);  // 256 threads -> 16 rows
   if (row_in_job >= J.n_rows) return;
   const int sub = threadIdx.x & 15;
-  float lse[kMaxMergeSrcs];
-  float mx = -CUDART_INF_F;
-  for (int i = 0; i < J.n_src; ++i) {
-    lse[i] = lse_arena[(int64_t)src_rows[J.src_begin + i] + row_in_job];
-    mx = fmaxf(mx, lse[i]);
-  }
+  // single pass over any number of partials: running max m, running sum of weights and a
+  // rescale of the accumulator whenever m grows (the LSE form of simexec.hpp:80-111)
   float acc[8];
 #pragma unroll
   for (int e = 0; e < 8; ++e) acc[e] = 0.f;
-  float lse_out = -CUDART_INF_F;
-  if (mx != -CUDART_INF_F) {
-    float denom = 0.f;
-    for (int i = 0; i < J.n_src; ++i) denom += lse[i] == -CUDART_INF_F ? 0.f : __expf(lse[i] - mx);
-    lse_out = mx + __logf(denom);
-    for (int i = 0; i < J.n_src; ++i) {
-      if (lse[i] == -CUDART_INF_F) continue;
-      const float w = __expf(lse[i] - mx) / denom;
-      const uint4 v = *(reinterpret_cast<const uint4*>(o_arena + ((int64_t)src_rows[J.src_begin + i] + row_in_job) * 128) + sub);
-      const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v);
+  float m = -CUDART_INF_F, denom = 0.f;
+  for (int i = 0; i < J.n_src; ++i) {
+    const int64_t row = (int64_t)src_rows[J.src_begin + i] + row_in_job;
+    const float l = lse_arena[row];
+    if (l == -CUDART_INF_F) continue;  // empty partial (l = 0 in the reference, :96-103)
+    if (l > m) {
+      const float c = __expf(m - l);  // m = -inf -> 0
+      denom *= c;
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        acc[2 * e] = fmaf(w, __bfloat162float(h[e].x), acc[2 * e]);
-        acc[2 * e + 1] = fmaf(w, __bfloat162float(h[e].y), acc[2 * e + 1]);
-      }
+      for (int e = 0; e < 8; ++e) acc[e] *= c;
+      m = l;
     }
+    const float w = __expf(l - m);
+    denom += w;
+    const uint4 v = *(reinterpret_cast<const uint4*>(o_arena + row * 128) + sub);
+    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      acc[2 * e] = fmaf(w, __bfloat162float(h[e].x), acc[2 * e]);
+      acc[2 * e + 1] = fmaf(w, __bfloat162float(h[e].y), acc[2 * e + 1]);
+    }
+  }
+  float lse_out = -CUDART_INF_F;
+  if (denom > 0.f) {
+    lse_out = m + __logf(denom);
+    const float inv = 1.f / denom;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) acc[e] *= inv;
   }
   __syncwarp();
   uint4 out;

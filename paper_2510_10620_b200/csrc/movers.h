@@ -10,7 +10,6 @@
 namespace dcpx {
 
 constexpr int kRowsPerChunk = 64;
-constexpr int kMaxMergeSrcs = 64;
 
 // Strided row copy: rows x row_bytes from src (stride src_stride) to dst. The launch
 // adds src_adjust / dst_adjust to every job's pointers, so jobs built at prepare time

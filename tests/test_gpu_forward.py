@@ -116,3 +116,17 @@ def test_deadlock_missing_sender():
     with pytest.raises(DCPXError) as ei:
         ex.prepare(bundle)
     assert ei.value.kind == "DeadlockError"
+
+
+def test_reduction_with_many_partials():
+    """ReductionInstr with more partials than a merge kernel would hold per thread (here 132,
+    simexec.hpp:80-111 takes any number): 132 kv tiles of block 64, unfused merge path."""
+    bundle = bundle_for([PL.SeqSpec(8448)], H=1, G=1, block=64, R=1, divisions=2)
+    nsrc = max(int(r[5]) for r in bundle.devices[0].instr if r[0] == 1)
+    assert nsrc > 64
+    (q, k, v), (q64, k64, v64) = inputs(bundle, seed=13)
+    o, lse, rep = _run_gpu(bundle, q, k, v, fuse=False, remap=False)
+    o_ref, lse_ref, orep, st, msg = O.run(bundle, q64, k64, v64)
+    assert st == 0, msg
+    assert rel_err(o, o_ref) <= O_TOL
+    assert lse_err(lse, lse_ref) <= LSE_TOL

@@ -1,0 +1,111 @@
+"""GPU, BASELINE.json configurations at full size (cached reference plans, plans/*.npz).
+
+Forward: every config's plan against dense FP64 masked attention (tests/oracle.hpp:80-120
+semantics) on sampled (token, head) rows, computed on the GPU from the same bf16 inputs;
+planned bytes and FLOPs bit-exact (CommVolume, BlockGraph::total_flops).
+Backward (no reference): plan invariance at full size -- the same inputs through the
+1-device and the 4-device plan of config 3 give the same O / LSE / dQ / dK / dV (the
+reference tests placement independence of the forward the same way,
+tests/test_simexec.cpp:210-222). Plan devices are spread over the GPUs present."""
+import os
+import sys
+
+import numpy as np
+import pytest
+
+from common import LSE_TOL, O_TOL, rel_err
+
+pytestmark = pytest.mark.gpu
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, os.path.join(REPO, "tools"))
+
+
+def _ngpu():
+    import torch
+    return torch.cuda.device_count()
+
+
+def _inputs(bundle, seed):
+    import torch
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    T, H, G = bundle.total_tokens, bundle.H, bundle.G
+    mk = lambda n: torch.randn((T, n, 128), device="cuda", generator=g).to(torch.bfloat16)  # noqa: E731
+    return mk(H), mk(G), mk(G), mk(H)
+
+
+def _dense_rows(bundle, q, k, v, toks, heads):
+    """FP64 masked attention for selected rows, on the GPU, from the bf16 inputs."""
+    import torch
+    G, H = bundle.G, bundle.H
+    seq_of = np.searchsorted(bundle.seq_offsets, toks, side="right") - 1
+    outs, lses = [], []
+    for t, h, s in zip(toks, heads, seq_of):
+        off = int(bundle.seq_offsets[s])
+        r = bundle.ranges[t]
+        keys = torch.from_numpy(np.concatenate([np.arange(r[0], r[1]), np.arange(r[2], r[3])]) + off).cuda()
+        grp = int(h) * G // H
+        if keys.numel() == 0:
+            outs.append(np.zeros(128)); lses.append(-np.inf); continue
+        kk, vv = k[keys, grp].double(), v[keys, grp].double()
+        sc = kk @ q[int(t), int(h)].double() / np.sqrt(128.0)
+        lse = torch.logsumexp(sc, 0)
+        outs.append((torch.softmax(sc, 0) @ vv).cpu().numpy())
+        lses.append(float(lse))
+    return np.array(outs), np.array(lses)
+
+
+def _run(bundle, q, k, v, d_o=None):
+    import torch
+
+    from paper_2510_10620_b200.executor import DCPExecutor
+    ex = DCPExecutor([d % _ngpu() for d in range(bundle.R)])
+    ex.prepare(bundle)
+    T, H, G = bundle.total_tokens, bundle.H, bundle.G
+    o = torch.zeros((T, H, 128), dtype=torch.bfloat16, device="cuda")
+    lse = torch.zeros((H, T), device="cuda")
+    ex.load_inputs(q, k, v)
+    rep = ex.forward(o, lse)
+    grads = None
+    if d_o is not None:
+        dq, dk, dv = torch.zeros_like(q), torch.zeros_like(k), torch.zeros_like(v)
+        ex.backward(d_o, dq, dk, dv)
+        grads = (dq, dk, dv)
+    ex.synchronize()
+    ex.close()
+    return o, lse, rep, grads
+
+
+@pytest.mark.parametrize("name", ["cfg2_R1", "cfg3_R4", "cfg4_cb_B512_R8", "cfg4_cb_B1024_R8",
+                                  "cfg4_cb_B2048_R8", "cfg4_sq_B2048_R8"])
+def test_fullsize_forward_sampled_rows(name):
+    from make_plans import load
+    bundle = load(name)
+    q, k, v, _ = _inputs(bundle, seed=5)
+    o, lse, rep, _ = _run(bundle, q, k, v)
+    rng = np.random.default_rng(7)
+    toks = rng.integers(0, bundle.total_tokens, 48)
+    heads = rng.integers(0, bundle.H, 48)
+    o_ref, lse_ref = _dense_rows(bundle, q, k, v, toks, heads)
+    got = o[toks, heads].float().cpu().numpy()
+    assert rel_err(got, o_ref) <= O_TOL, name
+    lse_got = lse[heads, toks].cpu().numpy()
+    fin = np.isfinite(lse_ref)
+    assert np.array_equal(np.isfinite(lse_got), fin)
+    assert np.abs(lse_got[fin] - lse_ref[fin]).max() <= LSE_TOL * max(1.0, np.abs(lse_ref[fin]).max())
+    assert rep["total_bytes"] == int(bundle.volume[0]), name
+    assert rep["total_flops"] == int(bundle.total_flops), name
+
+
+def test_fullsize_backward_plan_invariance():
+    from make_plans import load
+    b1, b4 = load("cfg3_R1"), load("cfg3_R4")
+    assert b1.total_tokens == b4.total_tokens and int(b1.total_flops) == int(b4.total_flops)
+    q, k, v, d_o = _inputs(b1, seed=9)
+    o1, l1, _, g1 = _run(b1, q, k, v, d_o)
+    o4, l4, r4, g4 = _run(b4, q, k, v, d_o)
+    assert r4["total_bytes"] == int(b4.volume[0])
+    assert rel_err(o4.float().cpu().numpy(), o1.float().cpu().numpy()) <= 1e-2
+    fin = np.isfinite(l1.cpu().numpy())
+    assert np.abs(l4.cpu().numpy()[fin] - l1.cpu().numpy()[fin]).max() <= LSE_TOL
+    for a, b in zip(g4, g1):
+        assert rel_err(a.float().cpu().numpy(), b.float().cpu().numpy()) <= 1e-2
