@@ -154,11 +154,20 @@ def main():
 
     name = f"{args.config}_R{N}" if args.placement == "dcp" else f"{args.config}_{args.placement}_R{N}"
     metric = "masked attention fwd+bwd TFLOPS"
-    config = {"workload": f"{args.config}: 8B-GPT attention layer (32 q / 8 kv heads, d 128), causal, "
-                          "LongAlign-skewed 64K-token batch (6 seqs, 63,855 tokens), block 1024, T 4, "
-                          f"DCP plan for {N} device(s)", "global_batch_tokens": None, "heads": "32/8",
-              "block": 1024, "parallelism": f"{args.placement}{N}", "placement": args.placement,
-              "l2": "inputs larger than L2 (q alone 523 MB)"}
+    workloads = {  # BASELINE.json configs[1..3] (synth seed 42 -> make_batches)
+        "cfg2": ("causal, LongAlign-skewed 64K-token batch (6 seqs, 63,855 tokens)", 1024),
+        "cfg3": ("lambda (sink 64 + window 4096), 128K-token batch (5 seqs, 130,968 tokens)", 1024),
+        "cfg4_cb_B512": ("causal-blockwise (256, 2, 1, 1), 128K-token batch", 512),
+        "cfg4_cb_B1024": ("causal-blockwise (256, 2, 1, 1), 128K-token batch", 1024),
+        "cfg4_cb_B2048": ("causal-blockwise (256, 2, 1, 1), 128K-token batch", 2048),
+        "cfg4_sq_B2048": ("shared-question (4 answers x 20 %), 128K-token batch", 2048),
+    }
+    desc, block = workloads.get(args.config, (args.config, None))
+    config = {"workload": f"{args.config}: 8B-GPT attention layer (32 q / 8 kv heads, d 128), {desc}, "
+                          f"block {block}, T 4, {args.placement.upper()} plan for {N} device(s)",
+              "global_batch_tokens": None, "heads": "32/8", "block": block,
+              "parallelism": f"{args.placement}{N}", "placement": args.placement,
+              "l2": "inputs larger than L2"}
 
     if args.impl == "reference":
         if rank != 0:

@@ -58,6 +58,11 @@ CONFIGS = {
     "cfg4_cb_B512_R8": (synth("causal_blockwise", 131072, 131072, 0), 8, 512, {}),
     "cfg4_cb_B1024_R8": (synth("causal_blockwise", 131072, 131072, 0), 8, 1024, {}),
     "cfg4_cb_B2048_R8": (synth("causal_blockwise", 131072, 131072, 0), 8, 2048, {}),
+    # the same block sweep on one device (bench.py --config cfg4_cb_B512 etc.)
+    "cfg4_cb_B512_R1": (synth("causal_blockwise", 131072, 131072, 0), 1, 512, {}),
+    "cfg4_cb_B1024_R1": (synth("causal_blockwise", 131072, 131072, 0), 1, 1024, {}),
+    "cfg4_cb_B2048_R1": (synth("causal_blockwise", 131072, 131072, 0), 1, 2048, {}),
+    "cfg4_sq_B2048_R1": (synth("shared_question", 131072, 131072, 0), 1, 2048, {}),
 }
 
 
