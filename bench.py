@@ -133,6 +133,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="dcpx", choices=["dcpx", "reference"])
     ap.add_argument("--config", default="cfg2")
+    ap.add_argument("--sm-reserve", type=int, default=-1,
+                    help="SMs kept free of attention CTAs for transfer kernels (-1: executor default)")
     ap.add_argument("--placement", default="dcp", choices=["dcp", "ring", "zigzag"],
                     help="plan placement: DCP (default) or the paper's baselines (cfg2 only)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -223,6 +225,8 @@ def main():
 
     ex = DCPExecutor(list(range(N)))
     ex.set_option("kernel_timing", 1)
+    if args.sm_reserve >= 0:
+        ex.set_option("sm_reserve", args.sm_reserve)
     ex.prepare(bundle)
     # N > 1: the distributed layout (dcpx_*_dev) -- every GPU holds the packed Q/K/V/dO of
     # the batch in its own HBM and receives the output rows it owns, as in a training step
