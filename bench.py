@@ -133,6 +133,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="dcpx", choices=["dcpx", "reference"])
     ap.add_argument("--config", default="cfg2")
+    ap.add_argument("--opt", action="append", default=[],
+                    help="executor option key=value (repeatable), e.g. bwd_window=8")
     ap.add_argument("--sm-reserve", type=int, default=-1,
                     help="SMs kept free of attention CTAs for transfer kernels (-1: executor default)")
     ap.add_argument("--placement", default="dcp", choices=["dcp", "ring", "zigzag"],
@@ -227,6 +229,11 @@ def main():
     ex.set_option("kernel_timing", 1)
     if args.sm_reserve >= 0:
         ex.set_option("sm_reserve", args.sm_reserve)
+    for kv in args.opt:
+        key, _, val = kv.partition("=")
+        ex.set_option(key, int(val))
+    if args.opt:
+        config["executor_options"] = ",".join(args.opt)
     ex.prepare(bundle)
     # N > 1: the distributed layout (dcpx_*_dev) -- every GPU holds the packed Q/K/V/dO of
     # the batch in its own HBM and receives the output rows it owns, as in a training step
