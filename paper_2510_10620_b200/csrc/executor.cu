@@ -1009,7 +1009,25 @@ void Executor::compile_device(int d) {
         std::vector<BwdStep> bsteps;
         std::vector<int64_t> bcost;
         std::vector<std::pair<int64_t, int64_t>> bkey;
-        const int win = opt.bwd_window > 0 ? opt.bwd_window : (1 << 30);
+        // windowing pays off for long units only: count the steps of the whole-item units
+        // first and window (with q-window-major order) when they average enough steps;
+        // short units (very sparse masks) stay whole, longest first
+        int64_t whole_units = 0, whole_steps = 0;
+        for (const auto& [kv_slot, idxs] : by_kv) {
+          const auto& c0 = icl.at(idxs[0]);
+          for (int ks = 0; ks < c0.nks; ++ks) {
+            int64_t n = 0;
+            for (int idx : idxs) {
+              const auto& c = icl.at(idx);
+              for (int qt = 0; qt < c.n_qb; ++qt) n += c.cls_b[qt * c.nks + ks] != 0;
+            }
+            whole_units += n > 0;
+            whole_steps += n;
+          }
+        }
+        const bool windowed = opt.bwd_window > 0 && whole_steps >= int64_t{opt.bwd_window_min_steps} * whole_units;
+        const int win = windowed ? opt.bwd_window : (1 << 30);
+        const int border_mode = windowed ? opt.bwd_order : 0;
         for (const auto& [kv_slot, idxs] : by_kv) {
           const auto& f = P.items[idxs[0]];
           const int n_k = static_cast<int>(f.kv_end - f.kv_begin);
@@ -1059,9 +1077,9 @@ void Executor::compile_device(int d) {
         std::iota(border.begin(), border.end(), 0);
         // bwd_order 0: longest-first; 1: plan order (kv slot, sub-tile, q window);
         // 2: q window major, so consecutive units (one wave) share their Q / dO / dQ rows
-        if (opt.bwd_order == 0)
+        if (border_mode == 0)
           std::stable_sort(border.begin(), border.end(), [&](size_t a, size_t b) { return bcost[a] > bcost[b]; });
-        else if (opt.bwd_order == 2)
+        else if (border_mode == 2)
           std::stable_sort(border.begin(), border.end(), [&](size_t a, size_t b) {
             const int64_t wa = bkey[a].first / (int64_t{kBwdQRows} * std::min(win, 1 << 20));
             const int64_t wb = bkey[b].first / (int64_t{kBwdQRows} * std::min(win, 1 << 20));

@@ -129,10 +129,13 @@ struct Options {
   int sm_reserve = -1;        // SMs left free of attention CTAs for transfer kernels (-1: auto)
   // backward units: (kv sub-tile, window of bwd_window 64-row q tiles of one item), ordered
   // q-window-major (2) so concurrent CTAs share Q / dO / dQ rows in L2; 0 = longest first,
-  // 1 = plan order. Measured on B200 (bench, 20 steps): window 16 / order 2 is best
-  // (cfg2 790 -> 803, cfg3 686 -> 714 TFLOP/s vs whole-item units, longest first).
+  // 1 = plan order. Windows apply to instructions whose whole-item units average at least
+  // bwd_window_min_steps steps; shorter units stay whole, longest first. Measured on B200
+  // (bench): cfg2 798 -> 813, cfg4 shared-question 761 -> 814 TFLOP/s with windows;
+  // cfg4 causal-blockwise (49 steps per unit) 339 with windows vs 366 without.
   int bwd_order = 2;
   int bwd_window = 16;
+  int bwd_window_min_steps = 128;
 };
 
 class Executor;
