@@ -162,6 +162,25 @@ Executor::Executor(int ndev, const int* ordinals) : R_(ndev) {
   }
 }
 
+void Executor::await_peer_pulls() {
+  if (pulls_done_.empty() || R_ < 2) return;
+  for (int d = 0; d < R_; ++d) {
+    DeviceGuard g(dev_[d].ordinal);
+    for (int e = 0; e < R_; ++e)
+      if (e != d && dev_[e].ordinal != dev_[d].ordinal) CUDA_OK(cudaStreamWaitEvent(dev_[d].cs, pulls_done_[e], 0));
+  }
+}
+
+void Executor::mark_pulls_done() {
+  if (R_ < 2) return;
+  if (pulls_done_.empty())
+    for (int d = 0; d < R_; ++d) pulls_done_.push_back(staging_event(d));
+  for (int d = 0; d < R_; ++d) {
+    DeviceGuard g(dev_[d].ordinal);
+    CUDA_OK(cudaEventRecord(pulls_done_[d], dev_[d].ms));
+  }
+}
+
 cudaEvent_t Executor::staging_event(int d) {
   DeviceGuard g(dev_[d].ordinal);
   cudaEvent_t e;
@@ -1402,6 +1421,7 @@ void Executor::load_inputs(const void* const* q, const void* const* k, const voi
     std::fill(sk.begin(), sk.end(), buf + bq);
     std::fill(sv.begin(), sv.end(), buf + bq + bk);
   }
+  await_peer_pulls();  // resident slots may still be read by a peer's previous-call pull
   for (int d = 0; d < R_; ++d) {
     DevState& D = dev_[d];
     DeviceGuard gd(D.ordinal);
@@ -1431,6 +1451,7 @@ void Executor::forward(void* const* o_out, float* const* lse_out, dcpx_report* r
     DeviceGuard gd(D.ordinal);
     if (opt.timing) CUDA_OK(cudaEventRecord(D.t0, D.cs));
   }
+  await_peer_pulls();
   std::map<std::string, cudaEvent_t> send_ev, recv_ev;
   std::vector<cudaEvent_t> ready_ev(static_cast<size_t>(R_));
   for (int d = 0; d < R_; ++d) {  // resident Q / KV were scattered on cs before this call
@@ -1497,6 +1518,7 @@ void Executor::forward(void* const* o_out, float* const* lse_out, dcpx_report* r
         break;
     }
   }
+  mark_pulls_done();
   // output assembly (simexec.hpp:403-421) into the caller's packed buffers
   std::vector<char*> o_dev(static_cast<size_t>(R_)), l_dev(static_cast<size_t>(R_));
   for (int d = 0; d < R_; ++d) {
@@ -1653,6 +1675,7 @@ void Executor::backward(const void* const* d_o, void* const* dq, void* const* dk
     std::fill(ddk.begin(), ddk.end(), ddk[0] ? buf + 2 * bq : nullptr);
     std::fill(ddv.begin(), ddv.end(), ddv[0] ? buf + 2 * bq + bk : nullptr);
   }
+  await_peer_pulls();
   const float scale = static_cast<float>(1.0 / std::sqrt(static_cast<double>(g_.D)));
   for (int d = 0; d < R_; ++d) {
     DevState& D = dev_[d];
@@ -1747,6 +1770,7 @@ void Executor::backward(const void* const* d_o, void* const* dq, void* const* dk
         break;
     }
   }
+  mark_pulls_done();
   // all gradient returns land before the owners convert their accumulators
   {
     std::vector<cudaEvent_t> ev(static_cast<size_t>(R_));

@@ -225,6 +225,12 @@ class Executor {
   char* out_stage_ = nullptr;  // host-output staging on device 0 (forward_host, synchronous)
   cudaStream_t h2d_ = nullptr, d2h_ = nullptr;  // on device 0
   cudaEvent_t staging_event(int d);              // persistent (not from the per-call pool)
+  // pulls_done_[d]: recorded on device d's comm stream at the end of each pass (its last
+  // peer reads); every device waits for its peers' before writing slots in the next call,
+  // so a lagging peer never reads a slot that the next call is already rewriting
+  std::vector<cudaEvent_t> pulls_done_;
+  void await_peer_pulls();
+  void mark_pulls_done();
   std::vector<cudaEvent_t> staging_events_;
   std::vector<int> staging_event_dev_;
   bool fwd_done_ = false;
