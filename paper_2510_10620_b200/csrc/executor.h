@@ -12,17 +12,13 @@
 #include <vector>
 
 #include "../../include/dcpx.h"
+#include "host_util.h"
 #include "movers.h"
 #include "program.h"
 
 namespace dcpx {
 
 // Exception carrying a dcpx_status (mirrors the reference hierarchy, types.hpp:17-45).
-struct Failure : std::runtime_error {
-  dcpx_status code;
-  Failure(dcpx_status c, const std::string& m) : std::runtime_error(m), code(c) {}
-};
-
 struct Instr {
   int op = 0, division = 0, send = 0, peer = 0, dst = 0, count = 0;
   int64_t offset = 0;
@@ -246,5 +242,34 @@ class Executor {
   template <class J>
   JobList make_row_jobs(int d, const std::vector<J>& jobs, const std::vector<int>& rows, int rows_per_block);
 };
+
+
+// ---- member templates (used by compile.cu and executor.cu)
+template <class T>
+T* Executor::upload(int d, const std::vector<T>& v) {
+  if (v.empty()) return nullptr;
+  T* p = static_cast<T*>(alloc(d, v.size() * sizeof(T)));
+  DeviceGuard g(dev_[d].ordinal);
+  CUDA_OK(cudaMemcpy(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
+  return p;
+}
+
+template <class J>
+JobList Executor::make_row_jobs(int d, const std::vector<J>& jobs, const std::vector<int>& rows,
+                                int rows_per_block) {
+  JobList L;
+  std::vector<int32_t> job_of_block, first_chunk;
+  for (size_t j = 0; j < jobs.size(); ++j) {
+    first_chunk.push_back(static_cast<int32_t>(job_of_block.size()));
+    const int nb = (rows[j] + rows_per_block - 1) / rows_per_block;
+    for (int b = 0; b < nb; ++b) job_of_block.push_back(static_cast<int32_t>(j));
+  }
+  L.dj.jobs = upload(d, jobs);
+  L.dj.job_of_block = upload(d, job_of_block);
+  L.dj.first_chunk = upload(d, first_chunk);
+  L.dj.n_blocks = static_cast<int32_t>(job_of_block.size());
+  L.dj.n_jobs = static_cast<int32_t>(jobs.size());
+  return L;
+}
 
 }  // namespace dcpx

@@ -1,0 +1,470 @@
+// run.cu — execution side of the B200 DCP executor (see executor.cu): input scatter,
+// forward / backward issue in the recorded lockstep order (attention launches, merges,
+// copies, event-ordered LOCAL transfers on the comm streams), output gathers, host I/O
+// staging and the SimReport-shaped report.
+#include <cuda_bf16.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <numeric>
+#include <string>
+
+#include "executor.h"
+
+namespace dcpx {
+
+// ------------------------------------------------------------------------ execution
+void Executor::load_inputs(const void* const* q, const void* const* k, const void* const* v, bool host) {
+  if (!prepared_) throw Failure(DCPX_ERROR, "dcpx_load_inputs before dcpx_prepare");
+  const int64_t TT = g_.total_tokens();
+  std::vector<const void*> sq(q, q + R_), sk(k, k + R_), sv(v, v + R_);
+  int slot = -1;
+  if (host) {
+    // upload into staging slot k on the h2d stream once the slot's previous scatters are
+    // done; peers read it over NVLink. The call returns without waiting for the copy.
+    DevState& D0 = dev_[0];
+    DeviceGuard gd(D0.ordinal);
+    const size_t bq = TT * g_.H * 256, bk = TT * g_.G * 256;
+    slot = in_st_.next;
+    in_st_.next ^= 1;
+    char*& buf = in_st_.buf[slot];
+    if (!buf) buf = static_cast<char*>(alloc(0, bq + 2 * bk));
+    for (cudaEvent_t e : in_st_.free[slot]) CUDA_OK(cudaStreamWaitEvent(h2d_, e, 0));
+    CUDA_OK(cudaMemcpyAsync(buf, q[0], bq, cudaMemcpyHostToDevice, h2d_));
+    CUDA_OK(cudaMemcpyAsync(buf + bq, k[0], bk, cudaMemcpyHostToDevice, h2d_));
+    CUDA_OK(cudaMemcpyAsync(buf + bq + bk, v[0], bk, cudaMemcpyHostToDevice, h2d_));
+    if (!in_st_.up[slot]) in_st_.up[slot] = staging_event(0);
+    cudaEvent_t up = in_st_.up[slot];
+    CUDA_OK(cudaEventRecord(up, h2d_));
+    for (int d = 0; d < R_; ++d) {
+      DeviceGuard g2(dev_[d].ordinal);
+      CUDA_OK(cudaStreamWaitEvent(dev_[d].cs, up, 0));
+    }
+    std::fill(sq.begin(), sq.end(), buf);
+    std::fill(sk.begin(), sk.end(), buf + bq);
+    std::fill(sv.begin(), sv.end(), buf + bq + bk);
+  }
+  await_peer_pulls();  // resident slots may still be read by a peer's previous-call pull
+  for (int d = 0; d < R_; ++d) {
+    DevState& D = dev_[d];
+    DeviceGuard gd(D.ordinal);
+    launch_row_copy(D.scatter_q.dj, D.cs, reinterpret_cast<int64_t>(sq[d]), 0);
+    launch_row_copy(D.scatter_k.dj, D.cs, reinterpret_cast<int64_t>(sk[d]), 0);
+    launch_row_copy(D.scatter_v.dj, D.cs, reinterpret_cast<int64_t>(sv[d]), 0);
+    CUDA_OK(cudaGetLastError());
+  }
+  if (slot >= 0) {  // the slot is free again once every device has scattered from it
+    auto& fr = in_st_.free[slot];
+    if (fr.empty())
+      for (int d = 0; d < R_; ++d) fr.push_back(staging_event(d));
+    for (int d = 0; d < R_; ++d) {
+      DeviceGuard gd(dev_[d].ordinal);
+      CUDA_OK(cudaEventRecord(fr[d], dev_[d].cs));
+    }
+  }
+}
+
+void Executor::forward(void* const* o_out, float* const* lse_out, dcpx_report* rep, bool host) {
+  if (!prepared_) throw Failure(DCPX_ERROR, "dcpx_forward before dcpx_prepare");
+  const int64_t TT = g_.total_tokens();
+  for (auto& D : dev_) {
+    D.next_event = 0;
+    D.next_kev = 0;
+    D.launches = 0;
+    DeviceGuard gd(D.ordinal);
+    if (opt.timing) CUDA_OK(cudaEventRecord(D.t0, D.cs));
+  }
+  await_peer_pulls();
+  std::map<std::string, cudaEvent_t> send_ev, recv_ev;
+  std::vector<cudaEvent_t> ready_ev(static_cast<size_t>(R_));
+  for (int d = 0; d < R_; ++d) {  // resident Q / KV were scattered on cs before this call
+    DeviceGuard gd(dev_[d].ordinal);
+    ready_ev[d] = event(d);
+    CUDA_OK(cudaEventRecord(ready_ev[d], dev_[d].cs));
+  }
+  trace_begin();
+  DeviceCursor cursor;
+  for (const auto& [d, i] : fwd_live_) {
+    DevState& D = dev_[d];
+    Op& op = D.prog[i];
+    cursor.to(D.ordinal);
+    TraceScope ts(this, d, static_cast<int>(i), op.kind == OpKind::kCommWait ? D.ms : D.cs, 0, op);
+    switch (op.kind) {
+      case OpKind::kFwdAttn: {
+        if (!op.num_units) break;
+        FwdParams p{};
+        p.units = op.units; p.steps = op.steps; p.items = op.items; p.ranges = D.ranges;
+        p.o_arena = D.o; p.lse_arena = D.lse; p.num_units = op.num_units;
+        p.slot_rows = static_cast<int32_t>(D.slot_rows);
+        p.scale_log2 = static_cast<float>(1.4426950408889634 / std::sqrt(static_cast<double>(g_.D)));
+        std::pair<cudaEvent_t, cudaEvent_t> ke{};
+        if (opt.kernel_timing) { ke = kernel_events(d); CUDA_OK(cudaEventRecord(ke.first, D.cs)); }
+        launch_attn_fwd(D.tm_q, D.tm_kv, p, attn_grid(d, op.grid), D.cs);
+        if (opt.kernel_timing) CUDA_OK(cudaEventRecord(ke.second, D.cs));
+        ++D.launches;
+        break;
+      }
+      case OpKind::kMerge:
+        launch_merge(op.jobs.dj, op.src_rows, D.o, D.lse, D.cs);
+        ++D.launches;
+        break;
+      case OpKind::kCopy:
+        launch_row_copy(op.jobs.dj, D.cs);
+        ++D.launches;
+        break;
+      case OpKind::kCommLaunch: {
+        if (op.send && op.resident_only) {
+          send_ev[op.tag] = ready_ev[d];  // resident inputs: ready since load / preprocess
+        } else {
+          cudaEvent_t e = event(d);
+          CUDA_OK(cudaEventRecord(e, D.cs));
+          (op.send ? send_ev : recv_ev)[op.tag] = e;
+        }
+        break;
+      }
+      case OpKind::kCommWait: {
+        CUDA_OK(cudaStreamWaitEvent(D.ms, send_ev.at(op.tag), 0));
+        CUDA_OK(cudaStreamWaitEvent(D.ms, recv_ev.at(op.tag), 0));
+        ts.split(kTraceXfer);
+        if (opt.sm_transfers) {
+          launch_row_copy(op.jobs.dj, D.ms);
+          ++D.launches;
+        } else {
+          copy_engine(op.xfer, D.ms);
+        }
+        cudaEvent_t e = event(d);
+        CUDA_OK(cudaEventRecord(e, D.ms));
+        CUDA_OK(cudaStreamWaitEvent(D.cs, e, 0));
+        break;
+      }
+      case OpKind::kNop:
+        break;
+    }
+  }
+  mark_pulls_done();
+  // output assembly (simexec.hpp:403-421) into the caller's packed buffers
+  std::vector<char*> o_dev(static_cast<size_t>(R_)), l_dev(static_cast<size_t>(R_));
+  for (int d = 0; d < R_; ++d) {
+    o_dev[d] = static_cast<char*>(o_out ? o_out[d] : nullptr);
+    l_dev[d] = reinterpret_cast<char*>(lse_out ? lse_out[d] : nullptr);
+  }
+  const bool want_o = o_dev[0] != nullptr, want_l = l_dev[0] != nullptr;
+  if (host && (want_o || want_l)) {
+    if (!out_stage_) out_stage_ = static_cast<char*>(alloc(0, TT * g_.H * 256 + TT * g_.H * 4));
+    std::fill(o_dev.begin(), o_dev.end(), want_o ? out_stage_ : nullptr);
+    std::fill(l_dev.begin(), l_dev.end(), want_l ? out_stage_ + TT * g_.H * 256 : nullptr);
+  }
+  for (int d = 0; d < R_; ++d) {
+    DevState& D = dev_[d];
+    DeviceGuard gd(D.ordinal);
+    if (o_dev[d]) { launch_row_copy(D.gather_o.dj, D.cs, 0, reinterpret_cast<int64_t>(o_dev[d])); ++D.launches; }
+    if (l_dev[d]) { launch_row_copy(D.gather_lse.dj, D.cs, 0, reinterpret_cast<int64_t>(l_dev[d])); ++D.launches; }
+    if (opt.timing) CUDA_OK(cudaEventRecord(D.t1, D.cs));
+    CUDA_OK(cudaGetLastError());
+  }
+  if (host && (want_o || want_l)) {
+    DevState& D0 = dev_[0];
+    DeviceGuard gd(D0.ordinal);
+    for (int d = 1; d < R_; ++d) {
+      cudaEvent_t e = event(d);
+      DeviceGuard g2(dev_[d].ordinal);
+      CUDA_OK(cudaEventRecord(e, dev_[d].cs));
+      DeviceGuard g3(D0.ordinal);
+      CUDA_OK(cudaStreamWaitEvent(D0.cs, e, 0));
+    }
+    if (want_o) CUDA_OK(cudaMemcpyAsync(o_out[0], o_dev[0], TT * g_.H * 256, cudaMemcpyDeviceToHost, D0.cs));
+    if (want_l) CUDA_OK(cudaMemcpyAsync(lse_out[0], l_dev[0], TT * g_.H * 4, cudaMemcpyDeviceToHost, D0.cs));
+    CUDA_OK(cudaStreamSynchronize(D0.cs));
+  }
+  fill_report(rep, false);
+  fwd_done_ = true;
+}
+
+void Executor::fill_report(dcpx_report* rep, bool bwd) {
+  if (opt.trace) trace_collect();
+  if (!rep) return;
+  std::memset(rep, 0, sizeof(*rep));
+  rep->devices = R_;
+  rep->stages = static_cast<int32_t>(comm_bytes_.size());
+  std::vector<double> comp_t(comm_bytes_.size(), 0), comm_t(comm_bytes_.size(), 0);
+  for (size_t t = 0; t < comm_bytes_.size(); ++t) {
+    for (const auto& [link, bytes] : comm_bytes_[t]) {
+      if (!bwd) {
+        rep->total_bytes += bytes;
+        rep->per_device_send[link.first] += bytes;
+        rep->per_device_recv[link.second] += bytes;
+      }
+      comm_t[t] = std::max(comm_t[t], bytes ? 5e-6 + static_cast<double>(bytes) / 600e9 : 0.0);  // link_time, schedule.hpp:209-215
+    }
+    for (int d = 0; d < R_; ++d) {
+      rep->total_flops += comp_flops_[t][d];
+      comp_t[t] = std::max(comp_t[t], static_cast<double>(comp_flops_[t][d]) / 312e12);  // CostParams, schedule.hpp:173-175
+    }
+  }
+  // pipeline_makespan (schedule.hpp:192-207)
+  double start_prev = 0, finish = 0;
+  for (size_t t = 0; t < comm_t.size(); ++t) {
+    const double start = t == 0 ? 0 : std::max(finish, start_prev + comm_t[t]);
+    start_prev = start;
+    finish = start + comp_t[t];
+  }
+  rep->makespan = finish;
+  if (bwd) {
+    // backward: 5 GEMMs per attended pair vs 2 forward -> 2.5x FLOPs; planned bytes =
+    // (Q + dO out, dQ back) per Q fetch and (KV out, dK/dV back) per KV fetch
+    rep->total_flops = rep->total_flops / 2 * 5;
+    rep->makespan = 0;
+    for (int d = 0; d < R_; ++d) {
+      rep->per_device_send[d] = bwd_send_[d];
+      rep->per_device_recv[d] = bwd_recv_[d];
+      rep->total_bytes += bwd_send_[d];
+    }
+  }
+  rep->wire_bytes = rep->total_bytes;
+  for (int d = 0; d < R_; ++d) rep->kernel_launches += dev_[d].launches;
+  if (opt.kernel_timing) {
+    double mx = 0;
+    for (auto& D : dev_) {
+      DeviceGuard gd(D.ordinal);
+      double sum = 0;
+      for (size_t k = 0; k < D.next_kev; ++k) {
+        CUDA_OK(cudaEventSynchronize(D.kev[k].second));
+        float ms = 0;
+        CUDA_OK(cudaEventElapsedTime(&ms, D.kev[k].first, D.kev[k].second));
+        sum += ms;
+      }
+      rep->attn_launches += static_cast<int32_t>(D.next_kev);
+      rep->attn_ms_sum += sum;
+      mx = std::max(mx, sum);
+    }
+    rep->attn_ms = mx;
+  }
+  if (opt.timing) {
+    double mx = 0;
+    for (auto& D : dev_) {
+      DeviceGuard gd(D.ordinal);
+      CUDA_OK(cudaEventSynchronize(D.t1));
+      float ms = 0;
+      CUDA_OK(cudaEventElapsedTime(&ms, D.t0, D.t1));
+      mx = std::max<double>(mx, ms);
+    }
+    rep->device_ms = mx;
+  }
+}
+
+void Executor::backward(const void* const* d_o, void* const* dq, void* const* dk, void* const* dv,
+                        dcpx_report* rep, bool host) {
+  if (!prepared_) throw Failure(DCPX_ERROR, "dcpx_backward before dcpx_prepare");
+  if (!fwd_done_) throw Failure(DCPX_ERROR, "dcpx_backward needs a preceding dcpx_forward");
+  const int64_t TT = g_.total_tokens(), H = g_.H, G = g_.G;
+  const int T = R_ ? plans_[0].divisions : 0;
+  std::vector<const char*> ddo(static_cast<size_t>(R_));
+  std::vector<char*> ddq(static_cast<size_t>(R_)), ddk(static_cast<size_t>(R_)), ddv(static_cast<size_t>(R_));
+  for (int d = 0; d < R_; ++d) {
+    ddo[d] = static_cast<const char*>(d_o[d]);
+    ddq[d] = static_cast<char*>(dq ? dq[d] : nullptr);
+    ddk[d] = static_cast<char*>(dk ? dk[d] : nullptr);
+    ddv[d] = static_cast<char*>(dv ? dv[d] : nullptr);
+  }
+  const size_t bq = TT * H * 256, bk = TT * G * 256;
+  for (auto& D : dev_) {
+    D.next_event = 0;
+    D.next_kev = 0;
+    D.launches = 0;
+    DeviceGuard gd(D.ordinal);
+    if (opt.timing) CUDA_OK(cudaEventRecord(D.t0, D.cs));
+  }
+  int slot = -1;
+  if (host) {
+    // dO up on h2d_ into staging slot k (once the slot's previous downloads are done);
+    // dQ/dK/dV come back through the same slot on d2h_ at the end. Asynchronous.
+    DevState& D0 = dev_[0];
+    DeviceGuard gd(D0.ordinal);
+    slot = bwd_st_.next;
+    bwd_st_.next ^= 1;
+    char*& buf = bwd_st_.buf[slot];
+    if (!buf) buf = static_cast<char*>(alloc(0, 2 * bq + 2 * bk));
+    for (cudaEvent_t e : bwd_st_.free[slot]) CUDA_OK(cudaStreamWaitEvent(h2d_, e, 0));
+    CUDA_OK(cudaMemcpyAsync(buf, d_o[0], bq, cudaMemcpyHostToDevice, h2d_));
+    if (!bwd_st_.up[slot]) bwd_st_.up[slot] = staging_event(0);
+    cudaEvent_t up = bwd_st_.up[slot];
+    CUDA_OK(cudaEventRecord(up, h2d_));
+    for (int d = 0; d < R_; ++d) {
+      DeviceGuard g2(dev_[d].ordinal);
+      CUDA_OK(cudaStreamWaitEvent(dev_[d].cs, up, 0));
+    }
+    std::fill(ddo.begin(), ddo.end(), buf);
+    std::fill(ddq.begin(), ddq.end(), ddq[0] ? buf + bq : nullptr);
+    std::fill(ddk.begin(), ddk.end(), ddk[0] ? buf + 2 * bq : nullptr);
+    std::fill(ddv.begin(), ddv.end(), ddv[0] ? buf + 2 * bq + bk : nullptr);
+  }
+  await_peer_pulls();
+  const float scale = static_cast<float>(1.0 / std::sqrt(static_cast<double>(g_.D)));
+  for (int d = 0; d < R_; ++d) {
+    DevState& D = dev_[d];
+    DeviceGuard gd(D.ordinal);
+    const int64_t SR = D.slot_rows;
+    CUDA_OK(cudaMemsetAsync(D.dq_acc, 0, std::max<int64_t>(1, D.cap_q) * SR * 512, D.cs));
+    CUDA_OK(cudaMemsetAsync(D.dkv_acc, 0, std::max<int64_t>(1, D.cap_kv) * 2 * SR * 512, D.cs));
+    launch_row_copy(D.scatter_do.dj, D.cs, reinterpret_cast<int64_t>(ddo[d]), 0);
+    launch_delta(D.prep.dj, D.o, D.lse, D.d_o, D.delta, D.lse2, D.cs);
+    D.launches += 2;
+  }
+  // every device's accumulators are zeroed before any peer returns into them: a device's
+  // first gradient return waits for its peers' zeroing (not its attention)
+  std::vector<cudaEvent_t> zeroed(static_cast<size_t>(R_));
+  std::vector<char> zero_waited(static_cast<size_t>(R_), 0);
+  for (int d = 0; d < R_; ++d) {
+    DeviceGuard gd(dev_[d].ordinal);
+    zeroed[d] = event(d);
+    CUDA_OK(cudaEventRecord(zeroed[d], dev_[d].cs));
+  }
+  auto await_zeroed = [&](int d) {
+    if (zero_waited[d]) return;
+    zero_waited[d] = 1;
+    DeviceGuard gd(dev_[d].ordinal);
+    for (int e = 0; e < R_; ++e)
+      if (e != d) CUDA_OK(cudaStreamWaitEvent(dev_[d].cs, zeroed[e], 0));
+  };
+  std::map<std::string, cudaEvent_t> send_ev, recv_ev;
+  std::vector<cudaEvent_t> ready_ev(static_cast<size_t>(R_));
+  for (int d = 0; d < R_; ++d) {  // dO scattered, Delta / LSE prepared on cs
+    DeviceGuard gd(dev_[d].ordinal);
+    ready_ev[d] = event(d);
+    CUDA_OK(cudaEventRecord(ready_ev[d], dev_[d].cs));
+  }
+  trace_begin();
+  DeviceCursor cursor;
+  for (const auto& [d, i] : bwd_live_) {  // the output stage has no backward counterpart
+    DevState& D = dev_[d];
+    Op& op = D.prog[i];
+    cursor.to(D.ordinal);
+    TraceScope ts(this, d, static_cast<int>(i), op.kind == OpKind::kCommWait ? D.ms : D.cs, 1, op);
+    switch (op.kind) {
+      case OpKind::kFwdAttn: {
+        if (op.bnum_units) {
+          BwdParams p{};
+          p.units = op.bunits; p.steps = op.bsteps; p.items = op.bitems; p.ranges = D.ranges;
+          p.lse2 = D.lse2; p.delta = D.delta; p.dq_acc = D.dq_acc; p.dkv_acc = D.dkv_acc;
+          p.num_units = op.bnum_units;
+          p.slot_rows = static_cast<int32_t>(D.slot_rows);
+          p.scale_log2 = static_cast<float>(1.4426950408889634) * scale;
+          p.scale = scale;
+          p.debug_flags = opt.bwd_debug;
+          std::pair<cudaEvent_t, cudaEvent_t> ke{};
+          if (opt.kernel_timing) { ke = kernel_events(d); CUDA_OK(cudaEventRecord(ke.first, D.cs)); }
+          launch_attn_bwd(D.tm_q64, D.tm_do, D.tm_kv, D.tm_dq, D.tm_dkv, p, attn_grid(d, op.bgrid), D.cs);
+          if (opt.kernel_timing) CUDA_OK(cudaEventRecord(ke.second, D.cs));
+          ++D.launches;
+        }
+        if (op.ret.dj.n_blocks) {
+          await_zeroed(d);
+          launch_return_accum(op.ret.dj, D.cs);
+          ++D.launches;
+        }
+        break;
+      }
+      case OpKind::kCommLaunch: {
+        if (op.send && op.resident_only) {
+          send_ev[op.tag] = ready_ev[d];  // resident inputs: ready since load / preprocess
+        } else {
+          cudaEvent_t e = event(d);
+          CUDA_OK(cudaEventRecord(e, D.cs));
+          (op.send ? send_ev : recv_ev)[op.tag] = e;
+        }
+        break;
+      }
+      case OpKind::kCommWait: {
+        CUDA_OK(cudaStreamWaitEvent(D.ms, send_ev.at(op.tag), 0));
+        CUDA_OK(cudaStreamWaitEvent(D.ms, recv_ev.at(op.tag), 0));
+        ts.split(kTraceXfer);
+        if (opt.sm_transfers) {
+          launch_row_copy(op.bjobs.dj, D.ms);
+          ++D.launches;
+        } else {
+          copy_engine(op.bxfer, D.ms);
+        }
+        cudaEvent_t e = event(d);
+        CUDA_OK(cudaEventRecord(e, D.ms));
+        CUDA_OK(cudaStreamWaitEvent(D.cs, e, 0));
+        break;
+      }
+      default:
+        break;
+    }
+  }
+  mark_pulls_done();
+  // all gradient returns land before the owners convert their accumulators
+  {
+    std::vector<cudaEvent_t> ev(static_cast<size_t>(R_));
+    for (int d = 0; d < R_; ++d) {
+      DeviceGuard gd(dev_[d].ordinal);
+      ev[d] = event(d);
+      CUDA_OK(cudaEventRecord(ev[d], dev_[d].cs));
+    }
+    for (int d = 0; d < R_; ++d)
+      for (int e = 0; e < R_; ++e)
+        if (e != d) {
+          DeviceGuard gd(dev_[d].ordinal);
+          CUDA_OK(cudaStreamWaitEvent(dev_[d].cs, ev[e], 0));
+        }
+  }
+  for (int d = 0; d < R_; ++d) {
+    DevState& D = dev_[d];
+    DeviceGuard gd(D.ordinal);
+    if (ddq[d]) { launch_to_bf16(D.gather_dq.dj, D.dq_acc, reinterpret_cast<__nv_bfloat16*>(ddq[d]), D.cs); ++D.launches; }
+    if (ddk[d]) { launch_to_bf16(D.gather_dk.dj, D.dkv_acc, reinterpret_cast<__nv_bfloat16*>(ddk[d]), D.cs); ++D.launches; }
+    if (ddv[d]) { launch_to_bf16(D.gather_dv.dj, D.dkv_acc, reinterpret_cast<__nv_bfloat16*>(ddv[d]), D.cs); ++D.launches; }
+    if (opt.timing) CUDA_OK(cudaEventRecord(D.t1, D.cs));
+    CUDA_OK(cudaGetLastError());
+  }
+  if (host) {
+    DevState& D0 = dev_[0];
+    DeviceGuard gd(D0.ordinal);
+    for (int d = 0; d < R_; ++d) {  // every device's conversions into the slot are done
+      cudaEvent_t e = event(d);
+      {
+        DeviceGuard g2(dev_[d].ordinal);
+        CUDA_OK(cudaEventRecord(e, dev_[d].cs));
+      }
+      CUDA_OK(cudaStreamWaitEvent(d2h_, e, 0));
+    }
+    if (ddq[0]) CUDA_OK(cudaMemcpyAsync(dq[0], ddq[0], bq, cudaMemcpyDeviceToHost, d2h_));
+    if (ddk[0]) CUDA_OK(cudaMemcpyAsync(dk[0], ddk[0], bk, cudaMemcpyDeviceToHost, d2h_));
+    if (ddv[0]) CUDA_OK(cudaMemcpyAsync(dv[0], ddv[0], bk, cudaMemcpyDeviceToHost, d2h_));
+    auto& fr = bwd_st_.free[slot];
+    if (fr.empty()) fr.push_back(staging_event(0));
+    CUDA_OK(cudaEventRecord(fr[0], d2h_));
+  }
+  fill_report(rep, true);
+}
+
+void Executor::synchronize() {
+  for (auto& D : dev_) {
+    DeviceGuard gd(D.ordinal);
+    CUDA_OK(cudaStreamSynchronize(D.cs));
+    CUDA_OK(cudaStreamSynchronize(D.ms));
+  }
+  if (R_ > 0) {
+    DeviceGuard gd(dev_[0].ordinal);
+    if (h2d_) CUDA_OK(cudaStreamSynchronize(h2d_));
+    if (d2h_) CUDA_OK(cudaStreamSynchronize(d2h_));
+  }
+}
+
+void Executor::debug_arena(int d, int kind, void** ptr, int64_t* rows) {
+  if (d < 0 || d >= R_) throw Failure(DCPX_ERROR, "bad device");
+  const DevState& D = dev_[d];
+  *rows = D.slot_rows;
+  switch (kind) {
+    case 0: *ptr = D.q; break;
+    case 1: *ptr = D.kv; break;
+    case 2: *ptr = D.o; break;
+    case 3: *ptr = D.lse; break;
+    default: throw Failure(DCPX_ERROR, "bad arena kind");
+  }
+}
+
+}  // namespace dcpx
