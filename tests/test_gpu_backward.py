@@ -127,3 +127,25 @@ def test_async_host_io_double_buffered():
         for a, b in ((h["dq"], dq), (h["dk"], dk), (h["dv"], dv)):
             assert rel_err(a.float().numpy(), b.float().cpu().numpy()) <= 4e-3
     ex.close()
+
+
+@pytest.mark.parametrize("H,G,block", [(2, 2, 200), (3, 1, 96), (8, 8, 160)])
+def test_forward_backward_unusual_shapes(H, G, block):
+    """Plain multi-head (H = G) and multi-query (G = 1, odd H) attention, block sizes that are
+    not multiples of the 128-row tiles (slots padded to 128 rows): forward and backward
+    against the FP64 oracle, backward bytes equal to the builder's formula."""
+    specs = [PL.SeqSpec(611), PL.SeqSpec(300, "lambda", sink=17, window=90),
+             PL.SeqSpec(450, "causal_blockwise", block=50, window_blocks=2, sink_blocks=1, test_blocks=1)]
+    bundle = bundle_for(specs, H=H, G=G, block=block, R=2)
+    (q, k, v), (q64, k64, v64) = inputs(bundle, seed=block)
+    d_o = _d_o(bundle, block)
+    (o, dq, dk, dv), rep = _fwd_bwd(bundle, q, k, v, d_o)
+    o_ref, lse_ref, orep, st, msg = O.run(bundle, q64, k64, v64)
+    assert st == 0, msg
+    assert rel_err(o, o_ref) <= O_TOL
+    rq, rk, rv = O.dense_backward(bundle, q64, k64, v64, d_o.double().numpy())
+    assert rel_err(dq, rq) <= O_TOL
+    assert rel_err(dk, rk) <= O_TOL
+    assert rel_err(dv, rv) <= O_TOL
+    send, recv = bundle.bwd_bytes()
+    assert rep["per_device_send"] == [int(x) for x in send]
