@@ -108,8 +108,10 @@ class DCPExecutor:
     """One context executing the plans of `bundle`.
 
     devices: CUDA ordinals, one per plan device (LOCAL transport, one process). Several
-    plan devices may share one GPU (single-GPU emulation of an R-device plan). For one
-    process per GPU use ``rank``/``world``/``nccl_id`` (NCCL transport)."""
+    plan devices may share one GPU (single-GPU emulation of an R-device plan).
+    ``rank``/``world``/``nccl_id`` select the one-process-per-GPU transport of the C ABI
+    (dcpx_create_rank), which returns Unsupported in this version. Usable as a context
+    manager (``with DCPExecutor(...) as ex:``) to release device memory deterministically."""
 
     def __init__(self, devices: Optional[Sequence[int]] = None, rank: Optional[int] = None,
                  world: Optional[int] = None, nccl_id: Optional[bytes] = None, cuda_ordinal: int = 0):
@@ -128,6 +130,12 @@ class DCPExecutor:
         self._keep = None
 
     def __del__(self):
+        self.close()
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
         self.close()
 
     def close(self):
