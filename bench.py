@@ -133,6 +133,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="dcpx", choices=["dcpx", "reference"])
     ap.add_argument("--config", default="cfg2")
+    ap.add_argument("--transport", default="local", choices=["local", "nccl"],
+                    help="block exchange: local = copy kernels over NVLink peer memory, nccl = send/recv")
     ap.add_argument("--opt", action="append", default=[],
                     help="executor option key=value (repeatable), e.g. bwd_window=8")
     ap.add_argument("--sm-reserve", type=int, default=-1,
@@ -225,7 +227,8 @@ def main():
     lse = torch.empty((H, T), device="cuda")
     dq, dk, dv = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
 
-    ex = DCPExecutor(list(range(N)))
+    ex = DCPExecutor(list(range(N)), transport=args.transport)
+    config["transport"] = args.transport
     ex.set_option("kernel_timing", 1)
     if args.sm_reserve >= 0:
         ex.set_option("sm_reserve", args.sm_reserve)

@@ -60,6 +60,9 @@ typedef enum {
   DCPX_UNSUPPORTED = 7       /* shape the sm_100a kernels do not handle (e.g. D != 128) */
 } dcpx_status;
 
+/* Block exchange between the plan devices of one context: LOCAL = copy kernels reading
+ * the sender's slots over NVLink peer memory (default); NCCL = grouped ncclSend/ncclRecv
+ * per message (one GPU per plan device). Gradient returns are peer-memory adds in both. */
 typedef enum { DCPX_TRANSPORT_LOCAL = 0, DCPX_TRANSPORT_NCCL = 1 } dcpx_transport;
 
 /* ---- block graph view: blocks.hpp:19-85 ---------------------------------------- */

@@ -44,13 +44,9 @@ const char* dcpx_version(void) { return "dcpx 0.1 (sm_100a tcgen05)"; }
 dcpx_status dcpx_create(int ndev, const int* cuda_ordinals, dcpx_transport transport, dcpx_ctx** out) {
   if (!out) return DCPX_ERROR;
   *out = nullptr;
-  if (transport != DCPX_TRANSPORT_LOCAL) {
-    g_create_err = "dcpx_create: only the LOCAL transport is process-local; use dcpx_create_rank for NCCL";
-    return DCPX_ERROR;
-  }
   try {
     auto* c = new dcpx_ctx;
-    c->ex = new dcpx::Executor(ndev, cuda_ordinals);
+    c->ex = new dcpx::Executor(ndev, cuda_ordinals, static_cast<int>(transport));
     *out = c;
     return DCPX_OK;
   } catch (const dcpx::Failure& e) {

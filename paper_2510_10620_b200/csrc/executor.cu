@@ -31,7 +31,7 @@
 namespace dcpx {
 
 // ------------------------------------------------------------------------ lifetime
-Executor::Executor(int ndev, const int* ordinals) : R_(ndev) {
+Executor::Executor(int ndev, const int* ordinals, int transport) : R_(ndev), transport_(transport) {
   if (ndev < 1 || ndev > 64) throw Failure(DCPX_ERROR, "dcpx_create: 1..64 devices supported");
   ordinals_.assign(ordinals, ordinals + ndev);
   int count = 0;
@@ -73,6 +73,43 @@ Executor::Executor(int ndev, const int* ordinals) : R_(ndev) {
     CUDA_OK(cudaStreamCreateWithFlags(&h2d_, cudaStreamNonBlocking));
     CUDA_OK(cudaStreamCreateWithFlags(&d2h_, cudaStreamNonBlocking));
   }
+  if (transport_ == DCPX_TRANSPORT_NCCL) {
+    std::set<int> distinct(ordinals_.begin(), ordinals_.end());
+    if (static_cast<int>(distinct.size()) != R_)
+      throw Failure(DCPX_UNSUPPORTED, "NCCL transport needs one GPU per plan device");
+    comms_.assign(static_cast<size_t>(R_), nullptr);
+    const ncclResult_t r = ncclCommInitAll(comms_.data(), R_, ordinals_.data());
+    if (r != ncclSuccess) throw Failure(DCPX_CUDA_ERROR, std::string("ncclCommInitAll: ") + ncclGetErrorString(r));
+  } else if (transport_ != DCPX_TRANSPORT_LOCAL) {
+    throw Failure(DCPX_ERROR, "unknown transport");
+  }
+}
+
+// NCCL transport: one message = a group of send/recv pairs over its contiguous row
+// regions. The sender's comm stream waits for the data, the receiver's for its slots;
+// groups are issued in the global lockstep order on every stream, so the rendezvous
+// sends cannot deadlock.
+void Executor::nccl_transfer(int src, int dst, const std::vector<RowCopyJob>& jobs, cudaEvent_t data_ready,
+                             cudaEvent_t slot_free) {
+  {
+    DeviceGuard g(dev_[src].ordinal);
+    CUDA_OK(cudaStreamWaitEvent(dev_[src].ms, data_ready, 0));
+  }
+  {
+    DeviceGuard g(dev_[dst].ordinal);
+    CUDA_OK(cudaStreamWaitEvent(dev_[dst].ms, slot_free, 0));
+  }
+  auto ok = [](ncclResult_t r, const char* what) {
+    if (r != ncclSuccess) throw Failure(DCPX_CUDA_ERROR, std::string(what) + ": " + ncclGetErrorString(r));
+  };
+  ok(ncclGroupStart(), "ncclGroupStart");
+  for (const auto& j : jobs) {
+    if (j.src_stride != j.row_bytes && j.rows > 1) throw Failure(DCPX_UNSUPPORTED, "NCCL transport: strided transfer");
+    const size_t n = static_cast<size_t>(j.rows) * j.row_bytes;
+    ok(ncclSend(j.src, n, ncclUint8, dst, comms_[src], dev_[src].ms), "ncclSend");
+    ok(ncclRecv(j.dst, n, ncclUint8, src, comms_[dst], dev_[dst].ms), "ncclRecv");
+  }
+  ok(ncclGroupEnd(), "ncclGroupEnd");
 }
 
 void Executor::await_peer_pulls() {
@@ -118,6 +155,8 @@ Executor::~Executor() {
     DeviceGuard g(staging_event_dev_[i]);
     cudaEventDestroy(staging_events_[i]);
   }
+  for (auto c : comms_)
+    if (c) ncclCommDestroy(c);
   free_all();
   if (diag_) cudaFreeHost(diag_);
   for (auto& d : dev_) {

@@ -3,6 +3,7 @@
 
 #include <cuda.h>
 #include <cuda_runtime.h>
+#include <nccl.h>
 
 #include <array>
 #include <map>
@@ -154,7 +155,9 @@ class TraceScope {
 
 class Executor {
  public:
-  Executor(int ndev, const int* ordinals);
+  // transport: DCPX_TRANSPORT_LOCAL (copy kernels reading peer memory) or
+  // DCPX_TRANSPORT_NCCL (NCCL send/recv pairs, one GPU per plan device)
+  Executor(int ndev, const int* ordinals, int transport = DCPX_TRANSPORT_LOCAL);
   ~Executor();
   void prepare(int nplans, const dcpx_plan_view* plans, const dcpx_graph_view* g,
                const dcpx_mask_view* m);
@@ -203,6 +206,10 @@ class Executor {
   std::vector<DevState> dev_;
   // global issue order from the lockstep simulation: (device, op index)
   std::vector<std::pair<int, int>> order_;
+  int transport_ = DCPX_TRANSPORT_LOCAL;
+  std::vector<ncclComm_t> comms_;  // NCCL transport: one communicator per plan device
+  void nccl_transfer(int src, int dst, const std::vector<RowCopyJob>& jobs, cudaEvent_t data_ready,
+                     cudaEvent_t slot_free);
   std::vector<std::pair<int, int>> fwd_live_, bwd_live_;  // order_ without ops that launch nothing
   std::vector<void*> allocs_;  // (ordinal, ptr) freed in destructor
   std::vector<int> alloc_dev_;

@@ -125,14 +125,19 @@ void Executor::forward(void* const* o_out, float* const* lse_out, dcpx_report* r
         break;
       }
       case OpKind::kCommWait: {
-        CUDA_OK(cudaStreamWaitEvent(D.ms, send_ev.at(op.tag), 0));
-        CUDA_OK(cudaStreamWaitEvent(D.ms, recv_ev.at(op.tag), 0));
-        ts.split(kTraceXfer);
-        if (opt.sm_transfers) {
-          launch_row_copy(op.jobs.dj, D.ms);
-          ++D.launches;
+        if (transport_ == DCPX_TRANSPORT_NCCL) {
+          nccl_transfer(op.peer, d, op.xfer, send_ev.at(op.tag), recv_ev.at(op.tag));
+          cursor.to(D.ordinal);
         } else {
-          copy_engine(op.xfer, D.ms);
+          CUDA_OK(cudaStreamWaitEvent(D.ms, send_ev.at(op.tag), 0));
+          CUDA_OK(cudaStreamWaitEvent(D.ms, recv_ev.at(op.tag), 0));
+          ts.split(kTraceXfer);
+          if (opt.sm_transfers) {
+            launch_row_copy(op.jobs.dj, D.ms);
+            ++D.launches;
+          } else {
+            copy_engine(op.xfer, D.ms);
+          }
         }
         cudaEvent_t e = event(d);
         CUDA_OK(cudaEventRecord(e, D.ms));
@@ -377,14 +382,19 @@ void Executor::backward(const void* const* d_o, void* const* dq, void* const* dk
         break;
       }
       case OpKind::kCommWait: {
-        CUDA_OK(cudaStreamWaitEvent(D.ms, send_ev.at(op.tag), 0));
-        CUDA_OK(cudaStreamWaitEvent(D.ms, recv_ev.at(op.tag), 0));
-        ts.split(kTraceXfer);
-        if (opt.sm_transfers) {
-          launch_row_copy(op.bjobs.dj, D.ms);
-          ++D.launches;
+        if (transport_ == DCPX_TRANSPORT_NCCL) {
+          nccl_transfer(op.peer, d, op.bxfer, send_ev.at(op.tag), recv_ev.at(op.tag));
+          cursor.to(D.ordinal);
         } else {
-          copy_engine(op.bxfer, D.ms);
+          CUDA_OK(cudaStreamWaitEvent(D.ms, send_ev.at(op.tag), 0));
+          CUDA_OK(cudaStreamWaitEvent(D.ms, recv_ev.at(op.tag), 0));
+          ts.split(kTraceXfer);
+          if (opt.sm_transfers) {
+            launch_row_copy(op.bjobs.dj, D.ms);
+            ++D.launches;
+          } else {
+            copy_engine(op.bxfer, D.ms);
+          }
         }
         cudaEvent_t e = event(d);
         CUDA_OK(cudaEventRecord(e, D.ms));

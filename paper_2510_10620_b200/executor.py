@@ -107,14 +107,17 @@ def _ptrs(ts):
 class DCPExecutor:
     """One context executing the plans of `bundle`.
 
-    devices: CUDA ordinals, one per plan device (LOCAL transport, one process). Several
-    plan devices may share one GPU (single-GPU emulation of an R-device plan).
+    devices: CUDA ordinals, one per plan device (one process). Several plan devices may
+    share one GPU (single-GPU emulation of an R-device plan). transport: "local" (copy
+    kernels reading peer memory over NVLink) or "nccl" (NCCL send/recv per message, one
+    GPU per plan device).
     ``rank``/``world``/``nccl_id`` select the one-process-per-GPU transport of the C ABI
     (dcpx_create_rank), which returns Unsupported in this version. Usable as a context
     manager (``with DCPExecutor(...) as ex:``) to release device memory deterministically."""
 
     def __init__(self, devices: Optional[Sequence[int]] = None, rank: Optional[int] = None,
-                 world: Optional[int] = None, nccl_id: Optional[bytes] = None, cuda_ordinal: int = 0):
+                 world: Optional[int] = None, nccl_id: Optional[bytes] = None, cuda_ordinal: int = 0,
+                 transport: str = "local"):
         self._h = C.c_void_p()
         self.rank = rank
         if rank is not None:
@@ -124,7 +127,8 @@ class DCPExecutor:
         else:
             devices = list(devices or [0])
             arr = (C.c_int * len(devices))(*devices)
-            self._check(lib().dcpx_create(len(devices), arr, 0, C.byref(self._h)), create=True)
+            tr = {"local": 0, "p2p": 0, "nccl": 1}[transport]  # dcpx_transport
+            self._check(lib().dcpx_create(len(devices), arr, tr, C.byref(self._h)), create=True)
             self.ndev = len(devices)
         self.bundle: Optional[P.PlanBundle] = None
         self._keep = None

@@ -124,3 +124,45 @@ def test_baseline_placements_on_gpu(placement):
     assert lse_err(lse.cpu().numpy(), lse_ref) <= LSE_TOL
     assert rep["total_bytes"] == orep.total_bytes == int(bundle.volume[0])
     ex.close()
+
+
+@pytest.mark.parametrize("R", [2, 4])
+def test_nccl_transport(R):
+    """The NCCL transport (send/recv per message, grouped; one GPU per plan device) gives
+    the same forward as the LOCAL copy kernels bit for bit, and the backward to bf16
+    rounding; bytes bit-exact."""
+    if _ngpu() < R:
+        pytest.skip(f"needs {R} GPUs")
+    import torch
+
+    import oracle as O
+    from paper_2510_10620_b200.executor import DCPExecutor
+    bundle = bundle_for(MIXED_SPECS, H=4, G=2, block=256, R=R)
+    (q, k, v), (q64, k64, v64) = inputs(bundle, seed=17)
+    T = bundle.total_tokens
+    g = torch.Generator().manual_seed(19)
+    d_o = torch.randn((T, 4, 128), generator=g).to(torch.bfloat16)
+    outs = {}
+    for tr in ("local", "nccl"):
+        ex = DCPExecutor(list(range(R)), transport=tr)
+        ex.prepare(bundle)
+        o = torch.zeros((T, 4, 128), dtype=torch.bfloat16, device="cuda:0")
+        lse = torch.zeros((4, T), device="cuda:0")
+        dq = torch.zeros_like(o)
+        dk = torch.zeros((T, 2, 128), dtype=torch.bfloat16, device="cuda:0")
+        dv = torch.zeros_like(dk)
+        ex.load_inputs(q.cuda(), k.cuda(), v.cuda())
+        rep = ex.forward(o, lse)
+        ex.backward(d_o.cuda(), dq, dk, dv)
+        ex.synchronize()
+        outs[tr] = (o.float().cpu(), lse.cpu(), dq.float().cpu(), dk.float().cpu(), dv.float().cpu(),
+                    rep["total_bytes"])
+        ex.close()
+    a, b = outs["local"], outs["nccl"]
+    assert torch.equal(a[0], b[0]) and torch.equal(a[1], b[1])
+    for x, y in zip(a[2:5], b[2:5]):
+        assert rel_err(x.numpy(), y.numpy()) <= 4e-3
+    assert a[5] == b[5] == int(bundle.volume[0])
+    o_ref, lse_ref, _, st, msg = O.run(bundle, q64, k64, v64)
+    assert st == 0, msg
+    assert rel_err(b[0].numpy(), o_ref) <= O_TOL

@@ -18,6 +18,9 @@ REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 REF = "/root/reference/proj"
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+# NCCL: the copy torch bundles (same soname as the one torch loads in-process)
+NCCL_DIR = os.path.join(sys.prefix, "lib", f"python{sys.version_info.major}.{sys.version_info.minor}",
+                        "site-packages", "nvidia", "nccl")
 
 
 def _stale(target, sources):
@@ -56,10 +59,11 @@ def build_dcpx(force=False):
                 extra.append("-DDCPX_BWD_PROFILE")
             if os.environ.get("DCPX_VARIANT"):
                 extra += os.environ.get("DCPX_DEFS", "").split()
-            _run([NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
+            _run([NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", f"-I{NCCL_DIR}/include",
                   "-Xptxas", "-warn-spills", *extra, "-c", s, "-o", o])
         objs.append(o)
-    _run([NVCC, *ARCH, "-shared", "-o", out, *objs, "-lcudart"])
+    _run([NVCC, *ARCH, "-shared", "-o", out, *objs, "-lcudart", f"-L{NCCL_DIR}/lib", "-l:libnccl.so.2",
+          "-Xlinker", "-rpath", "-Xlinker", f"{NCCL_DIR}/lib"])
     return out
 
 
