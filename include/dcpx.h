@@ -169,17 +169,28 @@ typedef struct dcpx_ctx dcpx_ctx;
 dcpx_status dcpx_create(int ndev, const int* cuda_ordinals, dcpx_transport transport,
                         dcpx_ctx** out);
 
-/* One plan device per process (rank == plan device), NCCL point-to-point over
- * NVLink. nccl_unique_id points to the 128-byte ncclUniqueId created by rank 0 and
- * broadcast by the caller (e.g. torch.distributed). */
-dcpx_status dcpx_create_rank(int rank, int world, int cuda_ordinal, const void* nccl_unique_id,
-                             dcpx_ctx** out);
+/* One plan device per process (rank == plan device) on CUDA device cuda_ordinal: the
+ * one-process-per-GPU deployment. Every rank prepares with ALL `world` plans (the
+ * receiver of a transfer needs the sender's slot layout), then exchanges its arena
+ * handles with the others:
+ *     dcpx_create_rank(rank, world, ordinal, &ctx); dcpx_prepare(ctx, world, plans, ...);
+ *     dcpx_rank_export(ctx, blob, cap, &size);      -> all-gather the blobs (any channel,
+ *     dcpx_rank_connect(ctx, all_blobs, size);         e.g. torch.distributed), rank order
+ * Transfers are then pulls over NVLink from the peers' CUDA-IPC-mapped arenas; ordering
+ * across processes is by device-side epoch flags (no host round trip, no collective).
+ * Every rank must issue the same sequence of load_inputs / forward / backward calls.
+ * The I/O calls use this rank's buffers only (the _dev variants read entry [rank]). */
+dcpx_status dcpx_create_rank(int rank, int world, int cuda_ordinal, dcpx_ctx** out);
 
-/* Returns the 128-byte ncclUniqueId to broadcast (rank 0 calls this). */
-dcpx_status dcpx_nccl_unique_id(void* out128);
+/* Writes this rank's handle blob (after dcpx_prepare) into buf; *size = its length. With
+ * cap too small nothing is written and *size tells the length needed. */
+dcpx_status dcpx_rank_export(dcpx_ctx* ctx, void* buf, int64_t cap, int64_t* size);
 
-/* Ingests the plans. In LOCAL mode `plans` holds all ndev plans in device order; in
- * NCCL mode it holds exactly this rank's plan (plans[0].device == rank). Validates
+/* Maps the peers' arenas; blobs = world blobs of blob_size bytes each, in rank order
+ * (this rank's own entry is ignored). Required after every dcpx_prepare. */
+dcpx_status dcpx_rank_connect(dcpx_ctx* ctx, const void* blobs, int64_t blob_size);
+
+/* Ingests the plans: all ndev plans in device order (also per rank). Validates
  * shapes, slots and tag pairing, sizes the slot arenas from BufferLayout::capacity,
  * and compiles the instruction stream into the device program. */
 dcpx_status dcpx_prepare(dcpx_ctx* ctx, int nplans, const dcpx_plan_view* plans,

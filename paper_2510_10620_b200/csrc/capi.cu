@@ -3,6 +3,7 @@
 // (types.hpp:17-45); the message is kept per context (dcpx_last_error).
 #include <cstring>
 #include <string>
+#include <vector>
 
 #include "executor.h"
 
@@ -146,14 +147,35 @@ void dcpx_destroy(dcpx_ctx* ctx) {
 
 }  // extern "C"
 
-// ---- backward; NCCL transport entry points (implemented in nccl.cu once built) -----------
+// ---- backward; per-rank entry points ----------------------------------------------------
 extern "C" {
-dcpx_status dcpx_create_rank(int, int, int, const void*, dcpx_ctx** out) {
-  if (out) *out = nullptr;
-  g_create_err = "dcpx_create_rank: NCCL transport not built yet";
-  return DCPX_UNSUPPORTED;
+dcpx_status dcpx_create_rank(int rank, int world, int cuda_ordinal, dcpx_ctx** out) {
+  if (!out) return DCPX_ERROR;
+  *out = nullptr;
+  try {
+    if (world < 1 || rank < 0 || rank >= world) throw dcpx::Failure(DCPX_ERROR, "dcpx_create_rank: bad rank / world");
+    auto* c = new dcpx_ctx;
+    const std::vector<int> ords(static_cast<size_t>(world), cuda_ordinal);
+    c->ex = new dcpx::Executor(world, ords.data(), DCPX_TRANSPORT_LOCAL, rank);
+    *out = c;
+    return DCPX_OK;
+  } catch (const dcpx::Failure& e) {
+    g_create_err = e.what();
+    return e.code;
+  } catch (const std::exception& e) {
+    g_create_err = e.what();
+    return DCPX_ERROR;
+  }
 }
-dcpx_status dcpx_nccl_unique_id(void*) { return DCPX_UNSUPPORTED; }
+dcpx_status dcpx_rank_export(dcpx_ctx* ctx, void* buf, int64_t cap, int64_t* size) {
+  return guarded(ctx, [&](dcpx::Executor& ex) {
+    const int64_t n = ex.export_handles(buf, buf ? cap : 0);
+    if (size) *size = n;
+  });
+}
+dcpx_status dcpx_rank_connect(dcpx_ctx* ctx, const void* blobs, int64_t blob_size) {
+  return guarded(ctx, [&](dcpx::Executor& ex) { ex.connect(blobs, blob_size, ex.devices()); });
+}
 dcpx_status dcpx_backward(dcpx_ctx* ctx, const void* d_o, void* dq, void* dk, void* dv, dcpx_report* rep) {
   return guarded(ctx, [&](dcpx::Executor& ex) {
     ex.backward(same_for_all(ex, d_o).data(), same_for_all(ex, dq).data(), same_for_all(ex, dk).data(),

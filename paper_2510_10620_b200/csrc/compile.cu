@@ -203,25 +203,30 @@ void Executor::compile_device(int d) {
   // ---- 3. arenas (zero-initialised: stale rows stay finite) and tensor maps
   {
     DeviceGuard gd(D.ordinal);
-    D.q = static_cast<__nv_bfloat16*>(alloc(d, std::max<int64_t>(1, D.cap_q) * SR * 256));
-    D.kv = static_cast<__nv_bfloat16*>(alloc(d, std::max<int64_t>(1, D.cap_kv) * 2 * SR * 256));
-    D.o = static_cast<__nv_bfloat16*>(alloc(d, std::max<int64_t>(1, D.cap_o) * SR * 256));
-    D.lse = static_cast<float*>(alloc(d, std::max<int64_t>(1, D.cap_o) * SR * 4));
-    CUDA_OK(cudaMemset(D.q, 0, std::max<int64_t>(1, D.cap_q) * SR * 256));
-    CUDA_OK(cudaMemset(D.kv, 0, std::max<int64_t>(1, D.cap_kv) * 2 * SR * 256));
-    CUDA_OK(cudaMemset(D.o, 0, std::max<int64_t>(1, D.cap_o) * SR * 256));
-    CUDA_OK(cudaMemset(D.lse, 0, std::max<int64_t>(1, D.cap_o) * SR * 4));
+    // per-rank mode: a peer's arenas are mapped from its process at connect(); until then
+    // a placeholder (its tensor maps are never used here)
+    const bool own = local(d);
+    auto arena = [&](int64_t bytes) { return alloc(d, own ? static_cast<size_t>(bytes) : 256); };
+    auto zero = [&](void* p, int64_t bytes) { if (own) CUDA_OK(cudaMemset(p, 0, bytes)); };
+    D.q = static_cast<__nv_bfloat16*>(arena(std::max<int64_t>(1, D.cap_q) * SR * 256));
+    D.kv = static_cast<__nv_bfloat16*>(arena(std::max<int64_t>(1, D.cap_kv) * 2 * SR * 256));
+    D.o = static_cast<__nv_bfloat16*>(arena(std::max<int64_t>(1, D.cap_o) * SR * 256));
+    D.lse = static_cast<float*>(arena(std::max<int64_t>(1, D.cap_o) * SR * 4));
+    zero(D.q, std::max<int64_t>(1, D.cap_q) * SR * 256);
+    zero(D.kv, std::max<int64_t>(1, D.cap_kv) * 2 * SR * 256);
+    zero(D.o, std::max<int64_t>(1, D.cap_o) * SR * 256);
+    zero(D.lse, std::max<int64_t>(1, D.cap_o) * SR * 4);
     // backward arenas, parallel to the Q arena (dO, LSE*log2e, Delta, dQ accumulator)
     // and to the KV arena (dK / dV accumulators)
     const int64_t nq = std::max<int64_t>(1, D.cap_q), nkv = std::max<int64_t>(1, D.cap_kv);
-    D.d_o = static_cast<__nv_bfloat16*>(alloc(d, nq * SR * 256));
-    D.lse2 = static_cast<float*>(alloc(d, nq * SR * 4));
-    D.delta = static_cast<float*>(alloc(d, nq * SR * 4));
-    D.dq_acc = static_cast<float*>(alloc(d, nq * SR * 512));
-    D.dkv_acc = static_cast<float*>(alloc(d, nkv * 2 * SR * 512));
-    CUDA_OK(cudaMemset(D.d_o, 0, nq * SR * 256));
-    CUDA_OK(cudaMemset(D.lse2, 0, nq * SR * 4));
-    CUDA_OK(cudaMemset(D.delta, 0, nq * SR * 4));
+    D.d_o = static_cast<__nv_bfloat16*>(arena(nq * SR * 256));
+    D.lse2 = static_cast<float*>(arena(nq * SR * 4));
+    D.delta = static_cast<float*>(arena(nq * SR * 4));
+    D.dq_acc = static_cast<float*>(arena(nq * SR * 512));
+    D.dkv_acc = static_cast<float*>(arena(nkv * 2 * SR * 512));
+    zero(D.d_o, nq * SR * 256);
+    zero(D.lse2, nq * SR * 4);
+    zero(D.delta, nq * SR * 4);
     D.tm_do = make_tmap(D.d_o, nq * SR, kBwdQRows);
     D.tm_dq = make_tmap_f32(D.dq_acc, nq * SR, kBwdQRows);
     D.tm_q = make_tmap(D.q, std::max<int64_t>(1, D.cap_q) * SR);

@@ -31,7 +31,10 @@
 namespace dcpx {
 
 // ------------------------------------------------------------------------ lifetime
-Executor::Executor(int ndev, const int* ordinals, int transport) : R_(ndev), transport_(transport) {
+Executor::Executor(int ndev, const int* ordinals, int transport, int rank)
+    : R_(ndev), transport_(transport), rank_(rank) {
+  if (rank_ >= 0 && (rank_ >= ndev || transport != DCPX_TRANSPORT_LOCAL))
+    throw Failure(DCPX_ERROR, "per-rank mode: rank outside the plan, or a transport other than peer memory");
   if (ndev < 1 || ndev > 64) throw Failure(DCPX_ERROR, "dcpx_create: 1..64 devices supported");
   ordinals_.assign(ordinals, ordinals + ndev);
   int count = 0;
@@ -113,6 +116,13 @@ void Executor::nccl_transfer(int src, int dst, const std::vector<RowCopyJob>& jo
 }
 
 void Executor::await_peer_pulls() {
+  if (rank_ >= 0) {  // per-rank mode: the peers' pulls flag of the last pass
+    if (connected_ && pulls_epoch_ > 0) {
+      DeviceGuard g(dev_[rank_].ordinal);
+      flag_wait_peers(kFlagPulls, pulls_epoch_, dev_[rank_].cs);
+    }
+    return;
+  }
   if (pulls_done_.empty() || R_ < 2) return;
   for (int d = 0; d < R_; ++d) {
     DeviceGuard g(dev_[d].ordinal);
@@ -122,6 +132,12 @@ void Executor::await_peer_pulls() {
 }
 
 void Executor::mark_pulls_done() {
+  if (rank_ >= 0) {
+    DeviceGuard g(dev_[rank_].ordinal);
+    flag_set(kFlagPulls, dev_[rank_].ms);
+    pulls_epoch_ = epoch_;
+    return;
+  }
   if (R_ < 2) return;
   if (pulls_done_.empty())
     for (int d = 0; d < R_; ++d) pulls_done_.push_back(staging_event(d));
@@ -157,6 +173,8 @@ Executor::~Executor() {
   }
   for (auto c : comms_)
     if (c) ncclCommDestroy(c);
+  for (void* p : ipc_mapped_) cudaIpcCloseMemHandle(p);
+  if (flags_) cudaFree(flags_);
   free_all();
   if (diag_) cudaFreeHost(diag_);
   for (auto& d : dev_) {
@@ -304,6 +322,14 @@ void Executor::prepare(int nplans, const dcpx_plan_view* plans, const dcpx_graph
                        const dcpx_mask_view* mv) {
   if (nplans != R_) throw Failure(DCPX_ERROR, "run: plan count does not match topology");  // simexec.hpp:211
   synchronize();  // asynchronous host I/O of a previous plan may still be in flight
+  if (rank_ >= 0) {  // per-rank mode: the previous plan's peer mappings and flags
+    DeviceGuard g(dev_[rank_].ordinal);
+    for (void* p : ipc_mapped_) cudaIpcCloseMemHandle(p);
+    ipc_mapped_.clear();
+    if (flags_) cudaFree(flags_);
+    flags_ = nullptr;
+    connected_ = false;
+  }
   free_all();
   out_stage_ = nullptr;
   for (Staging* st : {&in_st_, &bwd_st_})
@@ -488,7 +514,116 @@ void Executor::prepare(int nplans, const dcpx_plan_view* plans, const dcpx_graph
     dev_[d].slot_rows = slot_rows;
     compile_device(d);
   }
-  // ---- LOCAL transport: precompiled transfer jobs, owned by the receiver
+  // ---- transfer jobs (owned by the receiver) and input / output jobs
+  build_transfer_jobs();
+  for (int d = 0; d < R_; ++d) build_io_jobs(d);
+  build_bwd_jobs();
+  for (int d = 0; d < R_; ++d) {
+    DeviceGuard g(dev_[d].ordinal);
+    CUDA_OK(cudaDeviceSynchronize());
+  }
+  // enqueue orders per pass without the ops that launch nothing (fused reductions, remapped
+  // copies; the backward also skips the output stage and the forward-only merges / copies)
+  fwd_live_.clear();
+  bwd_live_.clear();
+  {
+    const int T = R_ ? plans_[0].divisions : 0;
+    for (const auto& [d, i] : order_) {
+      const Op& op = dev_[d].prog[i];
+      if (op.kind == OpKind::kNop) continue;
+      fwd_live_.push_back({d, i});
+      if (plans_[d].ins[i].division < T &&
+          (op.kind == OpKind::kFwdAttn || op.kind == OpKind::kCommLaunch || op.kind == OpKind::kCommWait))
+        bwd_live_.push_back({d, i});
+    }
+  }
+  if (rank_ >= 0) {  // per-rank mode: flags for the peers, tags numbered the same on every rank
+    tag_id_.clear();
+    for (const auto& P : plans_)
+      for (const auto& I : P.ins)
+        if (I.op == DCPX_OP_COMM_LAUNCH && I.send) tag_id_.emplace(I.tag, static_cast<int>(tag_id_.size()));
+    DeviceGuard g(dev_[rank_].ordinal);
+    const size_t words = kFlagSend + tag_id_.size();
+    CUDA_OK(cudaMalloc(&flags_, words * sizeof(uint32_t)));
+    CUDA_OK(cudaMemset(flags_, 0, words * sizeof(uint32_t)));
+    epoch_ = pulls_epoch_ = 0;
+    connected_ = false;
+  }
+  prepared_ = true;
+}
+
+// ---- per-rank mode ---------------------------------------------------------------------
+namespace {
+struct IpcBlob {
+  int32_t rank, n;
+  cudaIpcMemHandle_t h[10];
+};
+}  // namespace
+
+int64_t Executor::export_handles(void* buf, int64_t cap) const {
+  if (rank_ < 0 || !prepared_) throw Failure(DCPX_ERROR, "export_handles: per-rank context after prepare only");
+  if (cap < static_cast<int64_t>(sizeof(IpcBlob))) return static_cast<int64_t>(sizeof(IpcBlob));
+  const DevState& D = dev_[rank_];
+  DeviceGuard g(D.ordinal);
+  IpcBlob b{};
+  b.rank = rank_;
+  void* ptrs[10] = {D.q, D.kv, D.o, D.lse, D.d_o, D.lse2, D.delta, D.dq_acc, D.dkv_acc, flags_};
+  b.n = 10;
+  for (int i = 0; i < 10; ++i) CUDA_OK(cudaIpcGetMemHandle(&b.h[i], ptrs[i]));
+  std::memcpy(buf, &b, sizeof(b));
+  return static_cast<int64_t>(sizeof(b));
+}
+
+void Executor::connect(const void* blobs, int64_t blob_size, int world) {
+  if (rank_ < 0 || !prepared_) throw Failure(DCPX_ERROR, "connect: per-rank context after prepare only");
+  if (world != R_ || blob_size != static_cast<int64_t>(sizeof(IpcBlob)))
+    throw Failure(DCPX_ERROR, "connect: handle blobs do not match this context");
+  DeviceGuard g(dev_[rank_].ordinal);
+  peer_flags_.assign(static_cast<size_t>(R_), nullptr);
+  peer_flags_[rank_] = flags_;
+  for (int e = 0; e < R_; ++e) {
+    if (e == rank_) continue;
+    IpcBlob b;
+    std::memcpy(&b, static_cast<const char*>(blobs) + e * blob_size, sizeof(b));
+    if (b.rank != e || b.n != 10) throw Failure(DCPX_ERROR, "connect: blob order");
+    void* p[10];
+    for (int i = 0; i < 10; ++i) {
+      CUDA_OK(cudaIpcOpenMemHandle(&p[i], b.h[i], cudaIpcMemLazyEnablePeerAccess));
+      ipc_mapped_.push_back(p[i]);
+    }
+    DevState& E = dev_[e];  // from here on, peer e's arenas are its own, mapped
+    E.q = static_cast<__nv_bfloat16*>(p[0]);
+    E.kv = static_cast<__nv_bfloat16*>(p[1]);
+    E.o = static_cast<__nv_bfloat16*>(p[2]);
+    E.lse = static_cast<float*>(p[3]);
+    E.d_o = static_cast<__nv_bfloat16*>(p[4]);
+    E.lse2 = static_cast<float*>(p[5]);
+    E.delta = static_cast<float*>(p[6]);
+    E.dq_acc = static_cast<float*>(p[7]);
+    E.dkv_acc = static_cast<float*>(p[8]);
+    peer_flags_[e] = static_cast<uint32_t*>(p[9]);
+  }
+  build_transfer_jobs();
+  build_bwd_jobs();
+  CUDA_OK(cudaDeviceSynchronize());
+  connected_ = true;
+}
+
+void Executor::flag_set(int word, cudaStream_t s) { launch_flag_set(flags_ + word, epoch_, s); }
+
+// Waits until the flag word of every peer (or of one peer) reached `epoch`.
+void Executor::flag_wait_peers(int word, uint32_t epoch, cudaStream_t s, int only_peer) {
+  std::vector<const uint32_t*> f;
+  for (int e = 0; e < R_; ++e)
+    if (e != rank_ && (only_peer < 0 || e == only_peer)) f.push_back(peer_flags_[e] + word);
+  for (size_t i = 0; i < f.size(); i += 64)
+    launch_flag_wait(f.data() + i, static_cast<int>(std::min<size_t>(64, f.size() - i)), epoch, s);
+}
+
+// Transfer jobs of every CommWait, owned by the receiver (they read the sender's arenas:
+// peer memory across GPUs, or IPC-mapped peer memory in the per-rank mode).
+void Executor::build_transfer_jobs() {
+  const int64_t SR = R_ ? dev_[0].slot_rows : 0;
   for (int d = 0; d < R_; ++d) {
     for (auto& op : dev_[d].prog) {
       if (op.kind != OpKind::kCommWait) continue;
@@ -514,47 +649,25 @@ void Executor::prepare(int nplans, const dcpx_plan_view* plans, const dcpx_graph
         const auto& db = g_.data_blocks[rb.block];
         const int rows = static_cast<int>(db.tok_end - db.tok_begin);
         if (db.kind == DCPX_KIND_Q) {
-          jobs.push_back({reinterpret_cast<const char*>(A.q + sb.slot * slot_rows * 128),
-                          reinterpret_cast<char*>(B.q + rb.slot * slot_rows * 128), 256, 256, rows, 256});
+          jobs.push_back({reinterpret_cast<const char*>(A.q + sb.slot * SR * 128),
+                          reinterpret_cast<char*>(B.q + rb.slot * SR * 128), 256, 256, rows, 256});
         } else if (db.kind == DCPX_KIND_KV) {
           for (int h = 0; h < 2; ++h)
-            jobs.push_back({reinterpret_cast<const char*>(A.kv + (2 * sb.slot + h) * slot_rows * 128),
-                            reinterpret_cast<char*>(B.kv + (2 * rb.slot + h) * slot_rows * 128), 256, 256, rows, 256});
+            jobs.push_back({reinterpret_cast<const char*>(A.kv + (2 * sb.slot + h) * SR * 128),
+                            reinterpret_cast<char*>(B.kv + (2 * rb.slot + h) * SR * 128), 256, 256, rows, 256});
         } else {
           const int64_t so = A.o_phys[sb.slot], ro = B.o_phys[rb.slot];
-          jobs.push_back({reinterpret_cast<const char*>(A.o + so * slot_rows * 128),
-                          reinterpret_cast<char*>(B.o + ro * slot_rows * 128), 256, 256, rows, 256});
-          jobs.push_back({reinterpret_cast<const char*>(A.lse + so * slot_rows),
-                          reinterpret_cast<char*>(B.lse + ro * slot_rows), 4 * rows, 4 * rows, 1, 4 * rows});
+          jobs.push_back({reinterpret_cast<const char*>(A.o + so * SR * 128),
+                          reinterpret_cast<char*>(B.o + ro * SR * 128), 256, 256, rows, 256});
+          jobs.push_back({reinterpret_cast<const char*>(A.lse + so * SR),
+                          reinterpret_cast<char*>(B.lse + ro * SR), 4 * rows, 4 * rows, 1, 4 * rows});
         }
       }
       op.jobs = make_jobs(d, jobs);
       op.xfer = jobs;
       op.peer = src_dev;
     }
-    build_io_jobs(d);
   }
-  build_bwd_jobs();
-  for (int d = 0; d < R_; ++d) {
-    DeviceGuard g(dev_[d].ordinal);
-    CUDA_OK(cudaDeviceSynchronize());
-  }
-  // enqueue orders per pass without the ops that launch nothing (fused reductions, remapped
-  // copies; the backward also skips the output stage and the forward-only merges / copies)
-  fwd_live_.clear();
-  bwd_live_.clear();
-  {
-    const int T = R_ ? plans_[0].divisions : 0;
-    for (const auto& [d, i] : order_) {
-      const Op& op = dev_[d].prog[i];
-      if (op.kind == OpKind::kNop) continue;
-      fwd_live_.push_back({d, i});
-      if (plans_[d].ins[i].division < T &&
-          (op.kind == OpKind::kFwdAttn || op.kind == OpKind::kCommLaunch || op.kind == OpKind::kCommWait))
-        bwd_live_.push_back({d, i});
-    }
-  }
-  prepared_ = true;
 }
 
 void Executor::simulate_order() {

@@ -156,8 +156,14 @@ class TraceScope {
 class Executor {
  public:
   // transport: DCPX_TRANSPORT_LOCAL (copy kernels reading peer memory) or
-  // DCPX_TRANSPORT_NCCL (NCCL send/recv pairs, one GPU per plan device)
-  Executor(int ndev, const int* ordinals, int transport = DCPX_TRANSPORT_LOCAL);
+  // DCPX_TRANSPORT_NCCL (NCCL send/recv pairs, one GPU per plan device). rank >= 0: the
+  // per-rank mode (one process per GPU): all ordinals are this process's GPU, only plan
+  // device `rank` executes, peers' arenas are mapped over CUDA IPC (export / connect).
+  Executor(int ndev, const int* ordinals, int transport = DCPX_TRANSPORT_LOCAL, int rank = -1);
+  // per-rank mode: IPC handles of this rank's arenas and flags; map every peer's
+  int64_t export_handles(void* buf, int64_t cap) const;
+  void connect(const void* blobs, int64_t blob_size, int world);
+  bool local(int d) const { return rank_ < 0 || d == rank_; }
   ~Executor();
   void prepare(int nplans, const dcpx_plan_view* plans, const dcpx_graph_view* g,
                const dcpx_mask_view* m);
@@ -207,6 +213,21 @@ class Executor {
   // global issue order from the lockstep simulation: (device, op index)
   std::vector<std::pair<int, int>> order_;
   int transport_ = DCPX_TRANSPORT_LOCAL;
+  // per-rank mode: device-side epoch flags instead of cross-device events. Word layout of
+  // each rank's flag buffer: kFlagZeroed, kFlagReturns, kFlagPulls, then one word per
+  // message tag (send ready).
+  enum { kFlagZeroed = 0, kFlagReturns = 1, kFlagPulls = 2, kFlagSend = 3 };
+  int rank_ = -1;
+  bool connected_ = false;
+  uint32_t* flags_ = nullptr;
+  std::vector<uint32_t*> peer_flags_;  // [R_], this rank's own included
+  std::map<std::string, int> tag_id_;
+  uint32_t epoch_ = 0, pulls_epoch_ = 0;
+  std::vector<void*> ipc_mapped_;
+  void flag_set(int word, cudaStream_t s);
+  void flag_wait_peers(int word, uint32_t epoch, cudaStream_t s, int only_peer = -1);
+  void build_transfer_jobs();
+  void publish_resident_sends(const std::vector<std::pair<int, int>>& live);
   std::vector<ncclComm_t> comms_;  // NCCL transport: one communicator per plan device
   void nccl_transfer(int src, int dst, const std::vector<RowCopyJob>& jobs, cudaEvent_t data_ready,
                      cudaEvent_t slot_free);

@@ -211,7 +211,39 @@ __global__ void f32_to_bf16_kernel(const RowJob* __restrict__ jobs, const int32_
   *(reinterpret_cast<uint4*>(dst_base + J.b_row0 + (int64_t)r * J.b_stride) + sub) = out;
 }
 
+// ---------------------------------------------------------------------------- epoch flags
+__global__ void flag_set_kernel(uint32_t* flag, uint32_t epoch) {
+  __threadfence_system();
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(flag), "r"(epoch) : "memory");
+}
+
+struct FlagList {
+  const uint32_t* f[64];
+};
+
+__global__ void flag_wait_kernel(FlagList fl, int n, uint32_t epoch) {
+  const int i = threadIdx.x;
+  if (i < n) {
+    const long long t0 = clock64();
+    for (;;) {
+      uint32_t v;
+      asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(fl.f[i]) : "memory");
+      if (static_cast<int32_t>(v - epoch) >= 0) break;
+      __nanosleep(200);
+      if (clock64() - t0 > 100000000000LL) __trap();  // ~50 s: a peer never arrived
+    }
+  }
+  __syncthreads();
+}
+
 // ---------------------------------------------------------------------------- launchers
+void launch_flag_set(uint32_t* flag, uint32_t epoch, cudaStream_t s) { flag_set_kernel<<<1, 1, 0, s>>>(flag, epoch); }
+void launch_flag_wait(const uint32_t* const* flags, int n, uint32_t epoch, cudaStream_t s) {
+  if (n <= 0) return;
+  FlagList fl{};
+  for (int i = 0; i < n && i < 64; ++i) fl.f[i] = flags[i];
+  flag_wait_kernel<<<1, 64, 0, s>>>(fl, n, epoch);
+}
 void launch_row_copy(const DevJobs& j, cudaStream_t s, int64_t src_adjust, int64_t dst_adjust) {
   if (j.n_blocks)
     row_copy_kernel<<<j.n_blocks, 256, 0, s>>>(static_cast<const RowCopyJob*>(j.jobs), j.job_of_block,

@@ -54,4 +54,11 @@ void set_watchdog_buffer_bwd(uint32_t* diag);
 void launch_attn_fwd(const CUtensorMap& tm_q, const CUtensorMap& tm_kv, const FwdParams& p, int grid,
                      cudaStream_t stream);
 
+// Per-rank transport: device-side epoch flags in memory shared across processes (CUDA IPC).
+// flag_set publishes `epoch` after everything queued earlier on the stream (system-scope
+// release); flag_wait holds the stream until every flags[i * stride] >= epoch (acquire),
+// trapping after ~10 s instead of hanging the GPU.
+void launch_flag_set(uint32_t* flag, uint32_t epoch, cudaStream_t s);
+void launch_flag_wait(const uint32_t* const* flags, int n, uint32_t epoch, cudaStream_t s);
+
 }  // namespace dcpx

@@ -16,8 +16,21 @@
 namespace dcpx {
 
 // ------------------------------------------------------------------------ execution
+// Per-rank mode: sends of resident blocks are ready as soon as the inputs are, so their
+// flags go up at the start of the pass (the LOCAL transport gates them on ready_ev).
+void Executor::publish_resident_sends(const std::vector<std::pair<int, int>>& live) {
+  if (rank_ < 0) return;
+  DevState& D = dev_[rank_];
+  for (const auto& [d, i] : live) {
+    if (d != rank_) continue;
+    const Op& op = D.prog[i];
+    if (op.kind == OpKind::kCommLaunch && op.send && op.resident_only) flag_set(kFlagSend + tag_id_.at(op.tag), D.cs);
+  }
+}
+
 void Executor::load_inputs(const void* const* q, const void* const* k, const void* const* v, bool host) {
   if (!prepared_) throw Failure(DCPX_ERROR, "dcpx_load_inputs before dcpx_prepare");
+  if (rank_ >= 0 && !connected_) throw Failure(DCPX_ERROR, "dcpx_load_inputs: per-rank context not connected (dcpx_rank_connect)");
   const int64_t TT = g_.total_tokens();
   std::vector<const void*> sq(q, q + R_), sk(k, k + R_), sv(v, v + R_);
   int slot = -1;
@@ -39,6 +52,7 @@ void Executor::load_inputs(const void* const* q, const void* const* k, const voi
     cudaEvent_t up = in_st_.up[slot];
     CUDA_OK(cudaEventRecord(up, h2d_));
     for (int d = 0; d < R_; ++d) {
+      if (!local(d)) continue;
       DeviceGuard g2(dev_[d].ordinal);
       CUDA_OK(cudaStreamWaitEvent(dev_[d].cs, up, 0));
     }
@@ -48,6 +62,7 @@ void Executor::load_inputs(const void* const* q, const void* const* k, const voi
   }
   await_peer_pulls();  // resident slots may still be read by a peer's previous-call pull
   for (int d = 0; d < R_; ++d) {
+    if (!local(d)) continue;
     DevState& D = dev_[d];
     DeviceGuard gd(D.ordinal);
     launch_row_copy(D.scatter_q.dj, D.cs, reinterpret_cast<int64_t>(sq[d]), 0);
@@ -60,6 +75,7 @@ void Executor::load_inputs(const void* const* q, const void* const* k, const voi
     if (fr.empty())
       for (int d = 0; d < R_; ++d) fr.push_back(staging_event(d));
     for (int d = 0; d < R_; ++d) {
+      if (!local(d)) continue;
       DeviceGuard gd(dev_[d].ordinal);
       CUDA_OK(cudaEventRecord(fr[d], dev_[d].cs));
     }
@@ -68,25 +84,33 @@ void Executor::load_inputs(const void* const* q, const void* const* k, const voi
 
 void Executor::forward(void* const* o_out, float* const* lse_out, dcpx_report* rep, bool host) {
   if (!prepared_) throw Failure(DCPX_ERROR, "dcpx_forward before dcpx_prepare");
+  if (rank_ >= 0 && !connected_) throw Failure(DCPX_ERROR, "dcpx_forward: per-rank context not connected (dcpx_rank_connect)");
+  if (rank_ >= 0 && !connected_) throw Failure(DCPX_ERROR, "per-rank context: connect before forward");
   const int64_t TT = g_.total_tokens();
-  for (auto& D : dev_) {
+  for (int d = 0; d < R_; ++d) {
+    DevState& D = dev_[d];
     D.next_event = 0;
     D.next_kev = 0;
     D.launches = 0;
+    if (!local(d)) continue;
     DeviceGuard gd(D.ordinal);
     if (opt.timing) CUDA_OK(cudaEventRecord(D.t0, D.cs));
   }
   await_peer_pulls();
+  ++epoch_;
   std::map<std::string, cudaEvent_t> send_ev, recv_ev;
   std::vector<cudaEvent_t> ready_ev(static_cast<size_t>(R_));
   for (int d = 0; d < R_; ++d) {  // resident Q / KV were scattered on cs before this call
+    if (!local(d)) continue;
     DeviceGuard gd(dev_[d].ordinal);
     ready_ev[d] = event(d);
     CUDA_OK(cudaEventRecord(ready_ev[d], dev_[d].cs));
   }
+  publish_resident_sends(fwd_live_);
   trace_begin();
   DeviceCursor cursor;
   for (const auto& [d, i] : fwd_live_) {
+    if (!local(d)) continue;
     DevState& D = dev_[d];
     Op& op = D.prog[i];
     cursor.to(D.ordinal);
@@ -121,6 +145,7 @@ void Executor::forward(void* const* o_out, float* const* lse_out, dcpx_report* r
           cudaEvent_t e = event(d);
           CUDA_OK(cudaEventRecord(e, D.cs));
           (op.send ? send_ev : recv_ev)[op.tag] = e;
+          if (rank_ >= 0 && op.send) flag_set(kFlagSend + tag_id_.at(op.tag), D.cs);
         }
         break;
       }
@@ -129,7 +154,10 @@ void Executor::forward(void* const* o_out, float* const* lse_out, dcpx_report* r
           nccl_transfer(op.peer, d, op.xfer, send_ev.at(op.tag), recv_ev.at(op.tag));
           cursor.to(D.ordinal);
         } else {
-          CUDA_OK(cudaStreamWaitEvent(D.ms, send_ev.at(op.tag), 0));
+          if (rank_ >= 0)  // the sender is another process: its send flag for this epoch
+            flag_wait_peers(kFlagSend + tag_id_.at(op.tag), epoch_, D.ms, op.peer);
+          else
+            CUDA_OK(cudaStreamWaitEvent(D.ms, send_ev.at(op.tag), 0));
           CUDA_OK(cudaStreamWaitEvent(D.ms, recv_ev.at(op.tag), 0));
           ts.split(kTraceXfer);
           if (opt.sm_transfers) {
@@ -162,6 +190,7 @@ void Executor::forward(void* const* o_out, float* const* lse_out, dcpx_report* r
     std::fill(l_dev.begin(), l_dev.end(), want_l ? out_stage_ + TT * g_.H * 256 : nullptr);
   }
   for (int d = 0; d < R_; ++d) {
+    if (!local(d)) continue;
     DevState& D = dev_[d];
     DeviceGuard gd(D.ordinal);
     if (o_dev[d]) { launch_row_copy(D.gather_o.dj, D.cs, 0, reinterpret_cast<int64_t>(o_dev[d])); ++D.launches; }
@@ -173,6 +202,7 @@ void Executor::forward(void* const* o_out, float* const* lse_out, dcpx_report* r
     DevState& D0 = dev_[0];
     DeviceGuard gd(D0.ordinal);
     for (int d = 1; d < R_; ++d) {
+      if (!local(d)) continue;
       cudaEvent_t e = event(d);
       DeviceGuard g2(dev_[d].ordinal);
       CUDA_OK(cudaEventRecord(e, dev_[d].cs));
@@ -231,7 +261,9 @@ void Executor::fill_report(dcpx_report* rep, bool bwd) {
   for (int d = 0; d < R_; ++d) rep->kernel_launches += dev_[d].launches;
   if (opt.kernel_timing) {
     double mx = 0;
-    for (auto& D : dev_) {
+    for (int d = 0; d < R_; ++d) {
+      if (!local(d)) continue;
+      DevState& D = dev_[d];
       DeviceGuard gd(D.ordinal);
       double sum = 0;
       for (size_t k = 0; k < D.next_kev; ++k) {
@@ -248,7 +280,9 @@ void Executor::fill_report(dcpx_report* rep, bool bwd) {
   }
   if (opt.timing) {
     double mx = 0;
-    for (auto& D : dev_) {
+    for (int d = 0; d < R_; ++d) {
+      if (!local(d)) continue;
+      DevState& D = dev_[d];
       DeviceGuard gd(D.ordinal);
       CUDA_OK(cudaEventSynchronize(D.t1));
       float ms = 0;
@@ -262,6 +296,7 @@ void Executor::fill_report(dcpx_report* rep, bool bwd) {
 void Executor::backward(const void* const* d_o, void* const* dq, void* const* dk, void* const* dv,
                         dcpx_report* rep, bool host) {
   if (!prepared_) throw Failure(DCPX_ERROR, "dcpx_backward before dcpx_prepare");
+  if (rank_ >= 0 && !connected_) throw Failure(DCPX_ERROR, "dcpx_backward: per-rank context not connected (dcpx_rank_connect)");
   if (!fwd_done_) throw Failure(DCPX_ERROR, "dcpx_backward needs a preceding dcpx_forward");
   const int64_t TT = g_.total_tokens(), H = g_.H, G = g_.G;
   const int T = R_ ? plans_[0].divisions : 0;
@@ -274,10 +309,12 @@ void Executor::backward(const void* const* d_o, void* const* dq, void* const* dk
     ddv[d] = static_cast<char*>(dv ? dv[d] : nullptr);
   }
   const size_t bq = TT * H * 256, bk = TT * G * 256;
-  for (auto& D : dev_) {
+  for (int d = 0; d < R_; ++d) {
+    DevState& D = dev_[d];
     D.next_event = 0;
     D.next_kev = 0;
     D.launches = 0;
+    if (!local(d)) continue;
     DeviceGuard gd(D.ordinal);
     if (opt.timing) CUDA_OK(cudaEventRecord(D.t0, D.cs));
   }
@@ -297,6 +334,7 @@ void Executor::backward(const void* const* d_o, void* const* dq, void* const* dk
     cudaEvent_t up = bwd_st_.up[slot];
     CUDA_OK(cudaEventRecord(up, h2d_));
     for (int d = 0; d < R_; ++d) {
+      if (!local(d)) continue;
       DeviceGuard g2(dev_[d].ordinal);
       CUDA_OK(cudaStreamWaitEvent(dev_[d].cs, up, 0));
     }
@@ -306,8 +344,10 @@ void Executor::backward(const void* const* d_o, void* const* dq, void* const* dk
     std::fill(ddv.begin(), ddv.end(), ddv[0] ? buf + 2 * bq + bk : nullptr);
   }
   await_peer_pulls();
+  ++epoch_;
   const float scale = static_cast<float>(1.0 / std::sqrt(static_cast<double>(g_.D)));
   for (int d = 0; d < R_; ++d) {
+    if (!local(d)) continue;
     DevState& D = dev_[d];
     DeviceGuard gd(D.ordinal);
     const int64_t SR = D.slot_rows;
@@ -322,27 +362,36 @@ void Executor::backward(const void* const* d_o, void* const* dq, void* const* dk
   std::vector<cudaEvent_t> zeroed(static_cast<size_t>(R_));
   std::vector<char> zero_waited(static_cast<size_t>(R_), 0);
   for (int d = 0; d < R_; ++d) {
+    if (!local(d)) continue;
     DeviceGuard gd(dev_[d].ordinal);
     zeroed[d] = event(d);
     CUDA_OK(cudaEventRecord(zeroed[d], dev_[d].cs));
+    if (rank_ >= 0) flag_set(kFlagZeroed, dev_[d].cs);
   }
   auto await_zeroed = [&](int d) {
     if (zero_waited[d]) return;
     zero_waited[d] = 1;
     DeviceGuard gd(dev_[d].ordinal);
+    if (rank_ >= 0) {
+      flag_wait_peers(kFlagZeroed, epoch_, dev_[d].cs);
+      return;
+    }
     for (int e = 0; e < R_; ++e)
       if (e != d) CUDA_OK(cudaStreamWaitEvent(dev_[d].cs, zeroed[e], 0));
   };
   std::map<std::string, cudaEvent_t> send_ev, recv_ev;
   std::vector<cudaEvent_t> ready_ev(static_cast<size_t>(R_));
   for (int d = 0; d < R_; ++d) {  // dO scattered, Delta / LSE prepared on cs
+    if (!local(d)) continue;
     DeviceGuard gd(dev_[d].ordinal);
     ready_ev[d] = event(d);
     CUDA_OK(cudaEventRecord(ready_ev[d], dev_[d].cs));
   }
+  publish_resident_sends(bwd_live_);
   trace_begin();
   DeviceCursor cursor;
   for (const auto& [d, i] : bwd_live_) {  // the output stage has no backward counterpart
+    if (!local(d)) continue;
     DevState& D = dev_[d];
     Op& op = D.prog[i];
     cursor.to(D.ordinal);
@@ -378,6 +427,7 @@ void Executor::backward(const void* const* d_o, void* const* dq, void* const* dk
           cudaEvent_t e = event(d);
           CUDA_OK(cudaEventRecord(e, D.cs));
           (op.send ? send_ev : recv_ev)[op.tag] = e;
+          if (rank_ >= 0 && op.send) flag_set(kFlagSend + tag_id_.at(op.tag), D.cs);
         }
         break;
       }
@@ -386,7 +436,10 @@ void Executor::backward(const void* const* d_o, void* const* dq, void* const* dk
           nccl_transfer(op.peer, d, op.bxfer, send_ev.at(op.tag), recv_ev.at(op.tag));
           cursor.to(D.ordinal);
         } else {
-          CUDA_OK(cudaStreamWaitEvent(D.ms, send_ev.at(op.tag), 0));
+          if (rank_ >= 0)  // the sender is another process: its send flag for this epoch
+            flag_wait_peers(kFlagSend + tag_id_.at(op.tag), epoch_, D.ms, op.peer);
+          else
+            CUDA_OK(cudaStreamWaitEvent(D.ms, send_ev.at(op.tag), 0));
           CUDA_OK(cudaStreamWaitEvent(D.ms, recv_ev.at(op.tag), 0));
           ts.split(kTraceXfer);
           if (opt.sm_transfers) {
@@ -407,7 +460,12 @@ void Executor::backward(const void* const* d_o, void* const* dq, void* const* dk
   }
   mark_pulls_done();
   // all gradient returns land before the owners convert their accumulators
-  {
+  if (rank_ >= 0) {
+    DevState& D = dev_[rank_];
+    DeviceGuard gd(D.ordinal);
+    flag_set(kFlagReturns, D.cs);
+    flag_wait_peers(kFlagReturns, epoch_, D.cs);
+  } else {
     std::vector<cudaEvent_t> ev(static_cast<size_t>(R_));
     for (int d = 0; d < R_; ++d) {
       DeviceGuard gd(dev_[d].ordinal);
@@ -422,6 +480,7 @@ void Executor::backward(const void* const* d_o, void* const* dq, void* const* dk
         }
   }
   for (int d = 0; d < R_; ++d) {
+    if (!local(d)) continue;
     DevState& D = dev_[d];
     DeviceGuard gd(D.ordinal);
     if (ddq[d]) { launch_to_bf16(D.gather_dq.dj, D.dq_acc, reinterpret_cast<__nv_bfloat16*>(ddq[d]), D.cs); ++D.launches; }
@@ -434,6 +493,7 @@ void Executor::backward(const void* const* d_o, void* const* dq, void* const* dk
     DevState& D0 = dev_[0];
     DeviceGuard gd(D0.ordinal);
     for (int d = 0; d < R_; ++d) {  // every device's conversions into the slot are done
+      if (!local(d)) continue;
       cudaEvent_t e = event(d);
       {
         DeviceGuard g2(dev_[d].ordinal);

@@ -27,7 +27,7 @@ STATUS = {0: "OK", 1: "Error", 2: "DeadlockError", 3: "TagMismatchError", 4: "Bu
           5: "InfeasibleError", 6: "CudaError", 7: "Unsupported"}
 
 # Every symbol include/dcpx.h declares (checked by tests/test_capi_symbols.py).
-EXPORTS = ["dcpx_create", "dcpx_create_rank", "dcpx_nccl_unique_id", "dcpx_prepare",
+EXPORTS = ["dcpx_create", "dcpx_create_rank", "dcpx_rank_export", "dcpx_rank_connect", "dcpx_prepare",
            "dcpx_load_inputs", "dcpx_load_inputs_host", "dcpx_forward", "dcpx_forward_host",
            "dcpx_backward", "dcpx_backward_host", "dcpx_load_inputs_dev", "dcpx_forward_dev",
            "dcpx_backward_dev", "dcpx_synchronize", "dcpx_debug_arena",
@@ -52,14 +52,16 @@ def lib():
         L = C.CDLL(LIB_PATH)
         L.dcpx_last_error.restype = C.c_char_p
         L.dcpx_version.restype = C.c_char_p
-        for name in ("dcpx_create", "dcpx_create_rank", "dcpx_nccl_unique_id", "dcpx_prepare",
+        for name in ("dcpx_create", "dcpx_create_rank", "dcpx_rank_export", "dcpx_rank_connect", "dcpx_prepare",
                      "dcpx_load_inputs", "dcpx_load_inputs_host", "dcpx_forward",
                      "dcpx_forward_host", "dcpx_backward", "dcpx_backward_host",
                      "dcpx_load_inputs_dev", "dcpx_forward_dev", "dcpx_backward_dev",
                      "dcpx_synchronize", "dcpx_debug_arena", "dcpx_set_option"):
             getattr(L, name).restype = C.c_int
         L.dcpx_create.argtypes = [C.c_int, C.POINTER(C.c_int), C.c_int, C.POINTER(C.c_void_p)]
-        L.dcpx_create_rank.argtypes = [C.c_int, C.c_int, C.c_int, C.c_void_p, C.POINTER(C.c_void_p)]
+        L.dcpx_create_rank.argtypes = [C.c_int, C.c_int, C.c_int, C.POINTER(C.c_void_p)]
+        L.dcpx_rank_export.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.POINTER(C.c_int64)]
+        L.dcpx_rank_connect.argtypes = [C.c_void_p, C.c_void_p, C.c_int64]
         L.dcpx_prepare.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p]
         L.dcpx_load_inputs.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
         L.dcpx_load_inputs_host.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
@@ -77,7 +79,6 @@ def lib():
         L.dcpx_set_option.argtypes = [C.c_void_p, C.c_char_p, C.c_int64]
         L.dcpx_last_error.argtypes = [C.c_void_p]
         L.dcpx_destroy.argtypes = [C.c_void_p]
-        L.dcpx_nccl_unique_id.argtypes = [C.c_void_p]
         L.dcpx_trace.argtypes = [C.c_void_p, C.c_void_p, C.c_int]
         L.dcpx_trace.restype = C.c_int
         _lib = L
@@ -111,19 +112,20 @@ class DCPExecutor:
     share one GPU (single-GPU emulation of an R-device plan). transport: "local" (copy
     kernels reading peer memory over NVLink) or "nccl" (NCCL send/recv per message, one
     GPU per plan device).
-    ``rank``/``world``/``nccl_id`` select the one-process-per-GPU transport of the C ABI
-    (dcpx_create_rank), which returns Unsupported in this version. Usable as a context
-    manager (``with DCPExecutor(...) as ex:``) to release device memory deterministically."""
+    ``rank``/``world``/``cuda_ordinal`` select the one-process-per-GPU mode
+    (dcpx_create_rank): this process executes plan device ``rank``; ``prepare`` takes the
+    whole bundle and exchanges arena handles with the other ranks through
+    ``torch.distributed`` (initialised by the caller; any backend). Every rank must make
+    the same sequence of calls. Usable as a context manager (``with DCPExecutor(...) as
+    ex:``) to release device memory deterministically."""
 
     def __init__(self, devices: Optional[Sequence[int]] = None, rank: Optional[int] = None,
-                 world: Optional[int] = None, nccl_id: Optional[bytes] = None, cuda_ordinal: int = 0,
-                 transport: str = "local"):
+                 world: Optional[int] = None, cuda_ordinal: int = 0, transport: str = "local"):
         self._h = C.c_void_p()
         self.rank = rank
         if rank is not None:
-            buf = C.create_string_buffer(bytes(nccl_id), 128)
-            self._check(lib().dcpx_create_rank(rank, world, cuda_ordinal, buf, C.byref(self._h)), create=True)
-            self.ndev = 1
+            self._check(lib().dcpx_create_rank(rank, world, cuda_ordinal, C.byref(self._h)), create=True)
+            self.ndev = world
         else:
             devices = list(devices or [0])
             arr = (C.c_int * len(devices))(*devices)
@@ -161,6 +163,21 @@ class DCPExecutor:
         self._check(lib().dcpx_prepare(self._h, len(pv), pv, C.byref(g), C.byref(m)))
         self.bundle = bundle
         self._keep = (keep, g, m, pv)
+        if self.rank is not None:
+            self._connect()
+
+    def _connect(self):
+        """All-gathers the arena handle blobs of the ranks and maps the peers' arenas."""
+        import torch.distributed as dist
+        size = C.c_int64()
+        self._check(lib().dcpx_rank_export(self._h, None, 0, C.byref(size)))
+        blob = C.create_string_buffer(size.value)
+        self._check(lib().dcpx_rank_export(self._h, blob, size.value, C.byref(size)))
+        blobs = [None] * self.ndev
+        dist.all_gather_object(blobs, blob.raw)
+        allb = C.create_string_buffer(b"".join(blobs), size.value * self.ndev)
+        self._check(lib().dcpx_rank_connect(self._h, allb, size.value))
+        dist.barrier()  # every rank mapped every arena before anyone runs
 
     # Tensors, or lists with one tensor per plan device in that device's own memory
     # (the distributed layout: dcpx_*_dev; device d touches only the rows it owns).
