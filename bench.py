@@ -10,9 +10,10 @@ F_total = 3.5 * F_fwd.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl dcpx|reference] [--config cfg2]
 
-N > 1 (launched by torchrun): the multi-GPU plan is executed on N GPUs by rank 0's
-context, which owns all N devices (LOCAL transport: peer-to-peer copies over NVLink);
-timing is the max over the devices. Other ranks join the barriers only.
+N > 1 (launched by torchrun, default --mode rank): one process per GPU, rank r executes
+plan device r (dcpx_create_rank: peer arenas mapped over CUDA IPC, transfers are pulls
+over NVLink ordered by device-side flags); timing is the max over ranks. --mode single:
+rank 0's context owns all N devices and the other ranks join the barriers only.
 """
 from __future__ import annotations
 
@@ -126,6 +127,18 @@ def cpu_baseline(bundle, seconds_target=15.0):
             "seconds": sec, "flops": flops}
 
 
+def covered_tokens(bundle, d, key):
+    """Tokens of the packed layout covered by plan device d's resident blocks (`key`:
+    resident_q / resident_kv / resident_o): the rows a rank's host I/O copies."""
+    import numpy as np
+    mask = np.zeros(bundle.total_tokens, bool)
+    for r in getattr(bundle.devices[d], key):
+        db = bundle.data_blocks[int(r["block"])]
+        off = int(bundle.seq_offsets[int(db["seq"])])
+        mask[off + int(db["tok_begin"]):off + int(db["tok_end"])] = True
+    return int(mask.sum())
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -143,6 +156,8 @@ def main():
                     help="plan placement: DCP (default) or the paper's baselines (cfg2 only)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--mode", default="rank", choices=["rank", "single"],
+                    help="N > 1 under torchrun: one process per GPU (rank) or one process owning all GPUs")
 
     args = ap.parse_args()
 
@@ -157,6 +172,15 @@ def main():
     def barrier():
         if dist is not None:
             dist.barrier()
+
+    def reduce(x, op):
+        """max / sum of a float over the ranks (identity without torch.distributed)."""
+        if dist is None or not rank_mode:
+            return x
+        import torch
+        t = torch.tensor([float(x)], dtype=torch.float64)
+        dist.all_reduce(t, op={"max": dist.ReduceOp.MAX, "sum": dist.ReduceOp.SUM}[op])
+        return float(t.item())
 
     name = f"{args.config}_R{N}" if args.placement == "dcp" else f"{args.config}_{args.placement}_R{N}"
     metric = "masked attention fwd+bwd TFLOPS"
@@ -204,7 +228,8 @@ def main():
 
     import torch
 
-    if rank != 0:
+    rank_mode = world > 1 and args.mode == "rank"
+    if world > 1 and not rank_mode and rank != 0:
         barrier()   # bundle ready
         barrier()   # timed region start
         barrier()   # timed region end
@@ -217,7 +242,9 @@ def main():
     config["global_batch_tokens"] = T
     F_fwd = bundle.total_flops
     F_total = 3.5 * F_fwd
-    torch.cuda.set_device(0)
+    ordinal = int(os.environ.get("LOCAL_RANK", rank)) if rank_mode else 0
+    devs = [ordinal] if rank_mode else list(range(N))  # the GPUs this process drives
+    torch.cuda.set_device(ordinal)
     g = torch.Generator(device="cuda").manual_seed(0)
     q = torch.randn((T, H, 128), device="cuda", generator=g).to(torch.bfloat16)
     k = torch.randn((T, G, 128), device="cuda", generator=g).to(torch.bfloat16)
@@ -227,8 +254,15 @@ def main():
     lse = torch.empty((H, T), device="cuda")
     dq, dk, dv = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
 
-    ex = DCPExecutor(list(range(N)), transport=args.transport)
-    config["transport"] = args.transport
+    if rank_mode:
+        if world != N:
+            raise SystemExit("--mode rank needs --nproc-per-node == --gpus")
+        ex = DCPExecutor(rank=rank, world=world, cuda_ordinal=ordinal)
+        config["transport"] = "per-rank: CUDA IPC peer arenas, device-side flags"
+    else:
+        ex = DCPExecutor(list(range(N)), transport=args.transport)
+        config["transport"] = args.transport
+    config["processes"] = world if rank_mode else 1
     ex.set_option("kernel_timing", 1)
     if args.sm_reserve >= 0:
         ex.set_option("sm_reserve", args.sm_reserve)
@@ -241,14 +275,15 @@ def main():
     # N > 1: the distributed layout (dcpx_*_dev) -- every GPU holds the packed Q/K/V/dO of
     # the batch in its own HBM and receives the output rows it owns, as in a training step
     # where each GPU produced its own tokens; no input or output crosses NVLink.
-    if N > 1:
+    if N > 1 and not rank_mode:
         def per_dev(x, like=False):
             return [torch.empty_like(x, device=f"cuda:{d}") if like else x.to(f"cuda:{d}") for d in range(N)]
         io = dict(q=per_dev(q), k=per_dev(k), v=per_dev(v), d_o=per_dev(d_o), o=per_dev(o, True),
                   lse=per_dev(lse, True), dq=per_dev(dq, True), dk=per_dev(dk, True), dv=per_dev(dv, True))
     else:
         io = dict(q=q, k=k, v=v, d_o=d_o, o=o, lse=lse, dq=dq, dk=dk, dv=dv)
-    config["io_layout"] = "per-device packed buffers (dcpx_*_dev)" if N > 1 else "packed buffers on cuda:0"
+    config["io_layout"] = ("per-rank packed buffers in each GPU's HBM" if rank_mode else
+                           "per-device packed buffers (dcpx_*_dev)" if N > 1 else "packed buffers on cuda:0")
     barrier()
 
     def step():
@@ -259,14 +294,14 @@ def main():
 
     for _ in range(args.warmup):
         step()
-    for d in range(N):
+    for d in devs:
         torch.cuda.synchronize(d)
     barrier()
     fwd_ms, bwd_ms, fwd_k, bwd_k, launches = [], [], [], [], 0
-    with ClockSampler(list(range(N))) as clk:
-        starts = [torch.cuda.Event(enable_timing=True) for _ in range(N)]
-        ends = [torch.cuda.Event(enable_timing=True) for _ in range(N)]
-        for d in range(N):
+    with ClockSampler(list(range(N)) if rank == 0 else []) as clk:
+        starts = {d: torch.cuda.Event(enable_timing=True) for d in devs}
+        ends = {d: torch.cuda.Event(enable_timing=True) for d in devs}
+        for d in devs:
             with torch.cuda.device(d):
                 torch.cuda.synchronize(d)
                 starts[d].record()
@@ -275,18 +310,23 @@ def main():
             rf, rb = step()
             fwd_ms.append(rf["device_ms"]); bwd_ms.append(rb["device_ms"])
             fwd_k.append(rf["attn_ms_sum"]); bwd_k.append(rb["attn_ms_sum"])
-            launches += rf["kernel_launches"] + rb["kernel_launches"] + 3 * N  # + q/k/v scatters
-        for d in range(N):
+            launches += rf["kernel_launches"] + rb["kernel_launches"] + 3 * len(devs)  # + q/k/v scatters
+        for d in devs:
             with torch.cuda.device(d):
                 ends[d].record()
                 torch.cuda.synchronize(d)
         wall = time.perf_counter() - t0
-    barrier()
+        barrier()
     # executor events bracket each call on every device (max over devices); the torch events
-    # on the default stream bracket the whole region per device
-    total_ms = max(starts[d].elapsed_time(ends[d]) for d in range(N))
-    ms_step = max(total_ms / args.steps, (sum(fwd_ms) + sum(bwd_ms)) / args.steps)
+    # on the default stream bracket the whole region per device; max over ranks
+    total_ms = max(starts[d].elapsed_time(ends[d]) for d in devs)
+    ms_step = reduce(max(total_ms / args.steps, (sum(fwd_ms) + sum(bwd_ms)) / args.steps), "max")
+    wall = reduce(wall, "max")
     value = F_total / (ms_step * 1e-3) / 1e12
+    if rank_mode:  # GPU-time in the kernels and launches summed over the ranks
+        fwd_k = [reduce(sum(fwd_k) / len(fwd_k), "sum")]
+        bwd_k = [reduce(sum(bwd_k) / len(bwd_k), "sum")]
+        launches = int(reduce(launches, "sum"))
 
     # roofline of the dominant kernel (backward attention, K1b) and of the forward (K1):
     # algorithmic FLOPs of all launches / GPU-time summed over the devices' launches
@@ -341,17 +381,25 @@ def main():
         for _ in range(2):
             e2e_step()
         ex.synchronize()
+        if rank_mode:
+            barrier()
         t0 = time.perf_counter()
         ne = max(2, args.steps // 2)
         for _ in range(ne):
             e2e_step()
         ex.synchronize()
-        e_ms = (time.perf_counter() - t0) / ne * 1e3
+        e_ms = reduce((time.perf_counter() - t0) / ne * 1e3, "max")
+        if rank_mode:  # each rank copies the token rows of its own plan device
+            rows_q = sum(covered_tokens(bundle, d, "resident_q") for d in range(N))
+            rows_kv = sum(covered_tokens(bundle, d, "resident_kv") for d in range(N))
+        else:
+            rows_q = rows_kv = T
         e2e = {"value": F_total / (e_ms * 1e-3) / 1e12, "unit": "TFLOP/s", "ms_per_step": e_ms,
-               "h2d_bytes_per_step": int(sum(x.numel() * 2 for x in (hq, hk, hv, hdo))),
-               "d2h_bytes_per_step": int(sum(x.numel() * 2 for x in (hdq, hdk, hdv))),
+               "h2d_bytes_per_step": 2 * rows_q * H * 256 + 2 * rows_kv * G * 256,
+               "d2h_bytes_per_step": rows_q * H * 256 + 2 * rows_kv * G * 256,
                "path": "dcpx_load_inputs_host + dcpx_forward + dcpx_backward_host (pinned host buffers, "
-                       "asynchronous: uploads/downloads overlap compute across steps)"}
+                       "asynchronous: uploads/downloads overlap compute across steps"
+                       + ("; every rank copies only its plan device's token rows)" if rank_mode else ")")}
 
     cb = None
     if not args.no_cpu_baseline and N == 1:
@@ -370,7 +418,10 @@ def main():
             "detail": {"fwd_ms": sum(fwd_ms) / len(fwd_ms), "bwd_ms": sum(bwd_ms) / len(bwd_ms),
                        "F_fwd": F_fwd, "F_total": F_total, "wall_ms_per_step": wall / args.steps * 1e3,
                        "planned_fwd_bytes": int(bundle.volume[0])}}
-    print(json.dumps(line), flush=True)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if rank_mode:
+        barrier()  # no rank unmaps its arenas while a peer may still read them
     ex.close()
 
 

@@ -593,6 +593,24 @@ void Executor::build_io_jobs(int d) {
     gl.push_back({reinterpret_cast<const char*>(D.lse + phys * SR), reinterpret_cast<char*>((db.head * TT + tok) * 4),
                   4 * rows, 4 * rows, 1, 4 * rows});
   }
+  auto tok_ranges = [&](const std::vector<dcpx_block_slot>& res) {
+    std::vector<std::pair<int64_t, int64_t>> r;
+    for (const auto& x : res) {
+      const auto& db = g_.data_blocks[x.block];
+      const int64_t off = g_.seq_offsets[db.seq];
+      r.push_back({off + db.tok_begin, off + db.tok_end});
+    }
+    std::sort(r.begin(), r.end());
+    std::vector<std::pair<int64_t, int64_t>> m;
+    for (const auto& x : r) {
+      if (!m.empty() && x.first <= m.back().second) m.back().second = std::max(m.back().second, x.second);
+      else m.push_back(x);
+    }
+    return m;
+  };
+  D.tok_q = tok_ranges(P.res_q);
+  D.tok_kv = tok_ranges(P.res_kv);
+  D.tok_o = tok_ranges(P.res_o);
   D.scatter_q = make_jobs(d, sq);
   D.scatter_k = make_jobs(d, sk);
   D.scatter_v = make_jobs(d, sv);

@@ -99,6 +99,9 @@ struct DevState {
   CUtensorMap tm_q{}, tm_kv{};
   std::vector<Op> prog;
   JobList scatter_q, scatter_k, scatter_v, gather_o, gather_lse;
+  // packed token ranges [begin, end) of the resident Q / KV / O blocks (merged): the rows
+  // this device reads from / writes to the caller's packed buffers
+  std::vector<std::pair<int64_t, int64_t>> tok_q, tok_kv, tok_o;
   // backward arenas (parallel to Q / KV arenas) and their io jobs
   __nv_bfloat16* d_o = nullptr;
   float *lse2 = nullptr, *delta = nullptr, *dq_acc = nullptr, *dkv_acc = nullptr;
@@ -227,6 +230,11 @@ class Executor {
   void flag_set(int word, cudaStream_t s);
   void flag_wait_peers(int word, uint32_t epoch, cudaStream_t s, int only_peer = -1);
   void build_transfer_jobs();
+  // host I/O: the packed token ranges the local device(s) touch (everything in the
+  // single-process context; this rank's rows in the per-rank mode)
+  std::vector<std::pair<int64_t, int64_t>> host_ranges(int which) const;  // 0 Q, 1 KV, 2 O
+  static void copy_ranges(void* dst, const void* src, const std::vector<std::pair<int64_t, int64_t>>& r,
+                          int64_t row_bytes, cudaMemcpyKind kind, cudaStream_t s);
   void publish_resident_sends(const std::vector<std::pair<int, int>>& live);
   std::vector<ncclComm_t> comms_;  // NCCL transport: one communicator per plan device
   void nccl_transfer(int src, int dst, const std::vector<RowCopyJob>& jobs, cudaEvent_t data_ready,

@@ -28,6 +28,21 @@ void Executor::publish_resident_sends(const std::vector<std::pair<int, int>>& li
   }
 }
 
+std::vector<std::pair<int64_t, int64_t>> Executor::host_ranges(int which) const {
+  const int64_t TT = g_.total_tokens();
+  if (rank_ < 0) return {{0, TT}};  // the devices of one process together touch every row
+  const DevState& D = dev_[rank_];
+  return which == 0 ? D.tok_q : which == 1 ? D.tok_kv : D.tok_o;
+}
+
+void Executor::copy_ranges(void* dst, const void* src, const std::vector<std::pair<int64_t, int64_t>>& r,
+                           int64_t row_bytes, cudaMemcpyKind kind, cudaStream_t s) {
+  for (const auto& [b, e] : r)
+    if (e > b)
+      CUDA_OK(cudaMemcpyAsync(static_cast<char*>(dst) + b * row_bytes, static_cast<const char*>(src) + b * row_bytes,
+                              (e - b) * row_bytes, kind, s));
+}
+
 void Executor::load_inputs(const void* const* q, const void* const* k, const void* const* v, bool host) {
   if (!prepared_) throw Failure(DCPX_ERROR, "dcpx_load_inputs before dcpx_prepare");
   if (rank_ >= 0 && !connected_) throw Failure(DCPX_ERROR, "dcpx_load_inputs: per-rank context not connected (dcpx_rank_connect)");
@@ -45,9 +60,11 @@ void Executor::load_inputs(const void* const* q, const void* const* k, const voi
     char*& buf = in_st_.buf[slot];
     if (!buf) buf = static_cast<char*>(alloc(0, bq + 2 * bk));
     for (cudaEvent_t e : in_st_.free[slot]) CUDA_OK(cudaStreamWaitEvent(h2d_, e, 0));
-    CUDA_OK(cudaMemcpyAsync(buf, q[0], bq, cudaMemcpyHostToDevice, h2d_));
-    CUDA_OK(cudaMemcpyAsync(buf + bq, k[0], bk, cudaMemcpyHostToDevice, h2d_));
-    CUDA_OK(cudaMemcpyAsync(buf + bq + bk, v[0], bk, cudaMemcpyHostToDevice, h2d_));
+    // only the token rows this process's devices read (all of them in one process)
+    const auto rq = host_ranges(0), rkv = host_ranges(1);
+    copy_ranges(buf, q[0], rq, g_.H * 256, cudaMemcpyHostToDevice, h2d_);
+    copy_ranges(buf + bq, k[0], rkv, g_.G * 256, cudaMemcpyHostToDevice, h2d_);
+    copy_ranges(buf + bq + bk, v[0], rkv, g_.G * 256, cudaMemcpyHostToDevice, h2d_);
     if (!in_st_.up[slot]) in_st_.up[slot] = staging_event(0);
     cudaEvent_t up = in_st_.up[slot];
     CUDA_OK(cudaEventRecord(up, h2d_));
@@ -209,8 +226,13 @@ void Executor::forward(void* const* o_out, float* const* lse_out, dcpx_report* r
       DeviceGuard g3(D0.ordinal);
       CUDA_OK(cudaStreamWaitEvent(D0.cs, e, 0));
     }
-    if (want_o) CUDA_OK(cudaMemcpyAsync(o_out[0], o_dev[0], TT * g_.H * 256, cudaMemcpyDeviceToHost, D0.cs));
-    if (want_l) CUDA_OK(cudaMemcpyAsync(lse_out[0], l_dev[0], TT * g_.H * 4, cudaMemcpyDeviceToHost, D0.cs));
+    const auto ro = host_ranges(2);
+    if (want_o) copy_ranges(o_out[0], o_dev[0], ro, g_.H * 256, cudaMemcpyDeviceToHost, D0.cs);
+    if (want_l)  // LSE is head-major [H][T]: one strided copy per token range
+      for (const auto& [b, e] : ro)
+        if (e > b)
+          CUDA_OK(cudaMemcpy2DAsync(static_cast<char*>(static_cast<void*>(lse_out[0])) + b * 4, TT * 4, l_dev[0] + b * 4,
+                                    TT * 4, (e - b) * 4, g_.H, cudaMemcpyDeviceToHost, D0.cs));
     CUDA_OK(cudaStreamSynchronize(D0.cs));
   }
   fill_report(rep, false);
@@ -329,7 +351,7 @@ void Executor::backward(const void* const* d_o, void* const* dq, void* const* dk
     char*& buf = bwd_st_.buf[slot];
     if (!buf) buf = static_cast<char*>(alloc(0, 2 * bq + 2 * bk));
     for (cudaEvent_t e : bwd_st_.free[slot]) CUDA_OK(cudaStreamWaitEvent(h2d_, e, 0));
-    CUDA_OK(cudaMemcpyAsync(buf, d_o[0], bq, cudaMemcpyHostToDevice, h2d_));
+    copy_ranges(buf, d_o[0], host_ranges(0), g_.H * 256, cudaMemcpyHostToDevice, h2d_);
     if (!bwd_st_.up[slot]) bwd_st_.up[slot] = staging_event(0);
     cudaEvent_t up = bwd_st_.up[slot];
     CUDA_OK(cudaEventRecord(up, h2d_));
@@ -501,9 +523,10 @@ void Executor::backward(const void* const* d_o, void* const* dq, void* const* dk
       }
       CUDA_OK(cudaStreamWaitEvent(d2h_, e, 0));
     }
-    if (ddq[0]) CUDA_OK(cudaMemcpyAsync(dq[0], ddq[0], bq, cudaMemcpyDeviceToHost, d2h_));
-    if (ddk[0]) CUDA_OK(cudaMemcpyAsync(dk[0], ddk[0], bk, cudaMemcpyDeviceToHost, d2h_));
-    if (ddv[0]) CUDA_OK(cudaMemcpyAsync(dv[0], ddv[0], bk, cudaMemcpyDeviceToHost, d2h_));
+    const auto rq = host_ranges(0), rkv = host_ranges(1);
+    if (ddq[0]) copy_ranges(dq[0], ddq[0], rq, H * 256, cudaMemcpyDeviceToHost, d2h_);
+    if (ddk[0]) copy_ranges(dk[0], ddk[0], rkv, G * 256, cudaMemcpyDeviceToHost, d2h_);
+    if (ddv[0]) copy_ranges(dv[0], ddv[0], rkv, G * 256, cudaMemcpyDeviceToHost, d2h_);
     auto& fr = bwd_st_.free[slot];
     if (fr.empty()) fr.push_back(staging_event(0));
     CUDA_OK(cudaEventRecord(fr[0], d2h_));

@@ -17,6 +17,7 @@ def main():
     ap.add_argument("--out", required=True)
     ap.add_argument("--iters", type=int, default=3)
     ap.add_argument("--placement", default="dcp")
+    ap.add_argument("--host", action="store_true")
     args = ap.parse_args()
     import numpy as np
     import torch
@@ -40,12 +41,18 @@ def main():
     ex.prepare(bundle)
     outs = []
     for it in range(args.iters):
-        o = torch.zeros((T, 4, 128), dtype=torch.bfloat16, device=dev)
-        lse = torch.zeros((4, T), device=dev)
-        dq, dk, dv = torch.zeros_like(q), torch.zeros_like(k), torch.zeros_like(v)
-        ex.load_inputs(q, k, v)
-        rep = ex.forward(o, lse)
-        ex.backward(d_o, dq, dk, dv)
+        # the last call goes through the host I/O path (pinned buffers; this rank uploads and
+        # downloads only the token rows of its plan device)
+        host = args.host and it == args.iters - 1
+        where = "cpu" if host else dev
+        mk = (lambda x: torch.zeros(x.shape, dtype=x.dtype).pin_memory()) if host else torch.zeros_like
+        o = mk(torch.empty((T, 4, 128), dtype=torch.bfloat16, device=where))
+        lse = mk(torch.empty((4, T), device=where))
+        dq, dk, dv = mk(q), mk(k), mk(v)
+        src = [x.cpu().pin_memory() for x in (q, k, v, d_o)] if host else (q, k, v, d_o)
+        ex.load_inputs(*src[:3])
+        rep = ex.forward(o, lse, host=host)
+        ex.backward(src[3], dq, dk, dv, host=host)
         ex.synchronize()
         outs.append((o, lse, dq, dk, dv, rep))
     for tag, (o, lse, dq, dk, dv, rep) in (("first", outs[0]), ("last", outs[-1])):

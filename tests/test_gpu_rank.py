@@ -4,7 +4,8 @@ writes only the rows its plan device owns; their union must equal the single-pro
 context's output on the same plan and inputs (O and LSE bit for bit, gradients to bf16
 rounding: atomic accumulation order differs), on the first and on a repeated call (the
 cross-call hazards: peers still pulling the previous call's resident blocks, zeroed
-accumulators), and the planned bytes must be bit-exact. Ranks spread over the GPUs
+accumulators; with `host`, the last call through the host I/O path, where each rank
+copies only its own token rows), and the planned bytes must be bit-exact. Ranks spread over the GPUs
 present (several share a GPU on a 1-GPU box)."""
 import os
 import socket
@@ -51,12 +52,12 @@ def _single_process(R, placement):
                     dk=dk.float().cpu().numpy(), dv=dv.float().cpu().numpy()), rep, bundle
 
 
-@pytest.mark.parametrize("R,placement", [(2, "dcp"), (4, "dcp"), (4, "zigzag")])
-def test_rank_mode_matches_single_process(R, placement, tmp_path):
+@pytest.mark.parametrize("R,placement,host", [(2, "dcp", False), (4, "dcp", True), (4, "zigzag", False)])
+def test_rank_mode_matches_single_process(R, placement, host, tmp_path):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={R}",
            "--master-addr=127.0.0.1", f"--master-port={_free_port()}",
            os.path.join(HERE, "rank_worker.py"), "--out", str(tmp_path), "--iters", "3",
-           "--placement", placement]
+           "--placement", placement] + (["--host"] if host else [])
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=420)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     want, rep, bundle = _single_process(R, placement)
