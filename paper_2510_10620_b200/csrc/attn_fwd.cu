@@ -33,6 +33,9 @@ namespace dcpx {
 #define DCPX_SOFT_EXP_PAIRS 0
 #endif
 constexpr int kSoftExpPairs = DCPX_SOFT_EXP_PAIRS;
+// Also measured and not kept: row max / row sum as 4 independent chains instead of one
+// FMNMX3 / FADD chain (cfg2 7.51 vs 7.38 ms), and splitting the S load so the first half's
+// max overlaps the second half's tcgen05.ld (much slower: the loaded registers spill).
 
 constexpr int kFwdThreads = 384;
 constexpr int kFwdSmem = 6 * 32768 + 1024;  // Q0 Q1 K[2] V[2] + alignment slack

@@ -21,7 +21,8 @@ from typing import Optional, Sequence
 from . import plans as P
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libdcpx.so")
+# DCPX_LIB: an experiment build (tools/build.py DCPX_VARIANT) instead of the product library
+LIB_PATH = os.environ.get("DCPX_LIB") or os.path.join(_HERE, "libdcpx.so")
 
 STATUS = {0: "OK", 1: "Error", 2: "DeadlockError", 3: "TagMismatchError", 4: "BufferOverflowError",
           5: "InfeasibleError", 6: "CudaError", 7: "Unsupported"}
