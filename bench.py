@@ -242,7 +242,9 @@ def main():
     config["global_batch_tokens"] = T
     F_fwd = bundle.total_flops
     F_total = 3.5 * F_fwd
-    ordinal = int(os.environ.get("LOCAL_RANK", rank)) if rank_mode else 0
+    # (ranks beyond the GPUs present share them: a functional check of an N-rank plan on a
+    # smaller box; such a run is not a valid measurement)
+    ordinal = int(os.environ.get("LOCAL_RANK", rank)) % torch.cuda.device_count() if rank_mode else 0
     devs = [ordinal] if rank_mode else list(range(N))  # the GPUs this process drives
     torch.cuda.set_device(ordinal)
     g = torch.Generator(device="cuda").manual_seed(0)
@@ -298,7 +300,7 @@ def main():
         torch.cuda.synchronize(d)
     barrier()
     fwd_ms, bwd_ms, fwd_k, bwd_k, launches = [], [], [], [], 0
-    with ClockSampler(list(range(N)) if rank == 0 else []) as clk:
+    with ClockSampler(list(range(min(N, torch.cuda.device_count()))) if rank == 0 else []) as clk:
         starts = {d: torch.cuda.Event(enable_timing=True) for d in devs}
         ends = {d: torch.cuda.Event(enable_timing=True) for d in devs}
         for d in devs:

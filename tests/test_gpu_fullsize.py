@@ -75,7 +75,7 @@ def _run(bundle, q, k, v, d_o=None):
     return o, lse, rep, grads
 
 
-@pytest.mark.parametrize("name", ["cfg2_R1", "cfg3_R4", "cfg4_cb_B512_R8", "cfg4_cb_B1024_R8",
+@pytest.mark.parametrize("name", ["cfg1_R2", "cfg2_R1", "cfg3_R4", "cfg4_cb_B512_R8", "cfg4_cb_B1024_R8",
                                   "cfg4_cb_B2048_R8", "cfg4_sq_B2048_R8"])
 def test_fullsize_forward_sampled_rows(name):
     from make_plans import load

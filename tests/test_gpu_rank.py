@@ -52,7 +52,8 @@ def _single_process(R, placement):
                     dk=dk.float().cpu().numpy(), dv=dv.float().cpu().numpy()), rep, bundle
 
 
-@pytest.mark.parametrize("R,placement,host", [(2, "dcp", False), (4, "dcp", True), (4, "zigzag", False)])
+@pytest.mark.parametrize("R,placement,host", [(2, "dcp", False), (4, "dcp", True), (4, "zigzag", False),
+                                                (8, "dcp", False)])
 def test_rank_mode_matches_single_process(R, placement, host, tmp_path):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={R}",
            "--master-addr=127.0.0.1", f"--master-port={_free_port()}",
