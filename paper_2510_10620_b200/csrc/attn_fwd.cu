@@ -21,6 +21,8 @@
 #include <cuda_bf16.h>
 #include <math_constants.h>
 
+#include <cstdio>
+
 #include "program.h"
 #include "sm100.cuh"
 
@@ -36,6 +38,16 @@ constexpr int kSoftExpPairs = DCPX_SOFT_EXP_PAIRS;
 // Also measured and not kept: row max / row sum as 4 independent chains instead of one
 // FMNMX3 / FADD chain (cfg2 7.51 vs 7.38 ms), and splitting the S load so the first half's
 // max overlaps the second half's tcgen05.ld (much slower: the loaded registers spill).
+
+// Per-phase cycle counters of the softmax warps (-DDCPX_FWD_PROFILE builds only): warp 4
+// lane 0 of CTA 0 accumulates the cycles of each phase over its steps and prints them.
+#ifdef DCPX_FWD_PROFILE
+#define FWD_T(v) const long long v = clock64()
+#define FWD_ACC(i, a, b) fprof[i] += (b) - (a)
+#else
+#define FWD_T(v)
+#define FWD_ACC(i, a, b)
+#endif
 
 constexpr int kFwdThreads = 384;
 constexpr int kFwdSmem = 6 * 32768 + 1024;  // Q0 Q1 K[2] V[2] + alignment slack
@@ -178,6 +190,10 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
               issue_s(t, st);
               issued[t] = j;
             }
+          if (j == U.step_count - 1) {  // every S of the unit is issued: Q may be refilled
+            if (elect_one()) umma_commit(&bars.q_empty);
+            __syncwarp();
+          }
           mbar_wait(&bars.v_full[st], ph);
           tc_fence_after();
 #pragma unroll
@@ -211,7 +227,6 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           __syncwarp();
         }
         if (elect_one()) {
-          umma_commit(&bars.q_empty);
           for (int t = 0; t < 2; ++t)
             if (has[t]) umma_commit(&bars.o_full[t]);
         }
@@ -229,26 +244,44 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     const uint32_t lane_addr = tbase + ((uint32_t)((warp & 3) * 32) << 16);
     const uint32_t s_col = 128 * t, o_col = 256 + 128 * t;
     uint32_t cnt_s = 0, cnt_o = 0;
+#ifdef DCPX_FWD_PROFILE
+    long long fprof[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+    const long long fprof_t0 = clock64();
+#endif
     for (int u = blockIdx.x; u < p.num_units; u += gridDim.x) {
       const FwdUnit U = p.units[u];
       if (t == 1 && U.n_rows <= kTileRows) continue;
       const FwdStep* steps = p.steps + U.step_begin;
       const bool row_valid = (128 * t + r) < U.n_rows;
       const int64_t q_local = U.q_local0 + 128 * t + r;
+      const int64_t orow = (int64_t)U.out_row0 + 128 * t + r;
+      __nv_bfloat16* out = p.o_arena + orow * kHeadDim;
+      const bool merge = (U.flags & 1) != 0;
+      if (merge && row_valid) {  // the epilogue's merge operands: to L2 while the steps run
+        prefetch_l2(out);
+        prefetch_l2(out + 64);
+        prefetch_l2(p.lse_arena + orow);
+      }
       float m_used = -CUDART_INF_F;  // running max, log2 domain (lazily updated)
       float l = 0.f;
       bool has = false;
+#ifdef DCPX_FWD_PROFILE
+      bool has_prev = false;
+#endif
       for (int j = 0; j < U.step_count; ++j) {
         const FwdStep S = steps[j];
         const uint32_t cl = cls_of(S.cls, t);
         if (!cl) continue;
+        FWD_T(t0);
         mbar_wait(&bars.s_full[t], cnt_s & 1);
         ++cnt_s;
         tc_fence_after();
+        FWD_T(t1);
         uint32_t sraw[128];
 #pragma unroll
         for (int c = 0; c < 128; c += 32) tmem_ld32(lane_addr + s_col + c, sraw + c);
         tmem_wait_ld();
+        FWD_T(t2);
         float s[128];
 #pragma unroll
         for (int c = 0; c < 128; ++c) s[c] = __uint_as_float(sraw[c]);
@@ -278,6 +311,10 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         float mx = -CUDART_INF_F;
 #pragma unroll
         for (int c = 0; c < 128; ++c) mx = fmaxf(mx, s[c]);
+#ifdef DCPX_FWD_PROFILE
+        mx = __shfl_sync(0xffffffffu, mx, lane);  // materialise before the timestamp
+#endif
+        FWD_T(t3);
         const float m_new = mx * p.scale_log2;
         float alpha = 1.f;
         const bool need = m_new > m_used + kRescaleThreshold || (m_used == -CUDART_INF_F && m_new > -CUDART_INF_F);
@@ -316,20 +353,28 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           tmem_st16(lane_addr + s_col + (c >> 1), pk);
         }
         l += sum;
+        FWD_T(t4);
         tmem_wait_st();
         tc_fence_before();
         mbar_arrive(&bars.p_ready[t]);
         has = true;
+        FWD_T(t5);
+        FWD_ACC(0, t0, t1); FWD_ACC(1, t1, t2); FWD_ACC(2, t2, t3); FWD_ACC(3, t3, t4); FWD_ACC(4, t4, t5);
+#ifdef DCPX_FWD_PROFILE
+        ++fprof[5];
+        if (!has_prev) fprof[7] += t1 - t0;
+        has_prev = true;
+#endif
       }
-      // ---- epilogue: O / l, LSE, optional merge with the destination's current value
-      const int64_t orow = (int64_t)U.out_row0 + 128 * t + r;
-      __nv_bfloat16* out = p.o_arena + orow * kHeadDim;
+      FWD_T(te0);
+      // ---- epilogue: O / l, LSE, optional merge with the destination's current value.
+      // The merge operands were prefetched to L2 at the start of the unit.
+      float lse_prev = -CUDART_INF_F;
+      if (merge && row_valid) lse_prev = p.lse_arena[orow];
       const float lse_new = l > 0.f ? (m_used + __log2f(l)) * 0.69314718055994531f : -CUDART_INF_F;
       const float inv_l = l > 0.f ? 1.f / l : 0.f;
       float w_new = 1.f, w_prev = 0.f, lse_out = lse_new;
-      const bool merge = (U.flags & 1) != 0;
       if (merge && row_valid) {
-        const float lse_prev = p.lse_arena[orow];
         const float mm = fmaxf(lse_new, lse_prev);
         if (mm == -CUDART_INF_F) {
           w_new = 0.f; w_prev = 0.f; lse_out = -CUDART_INF_F;
@@ -391,7 +436,18 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         tc_fence_before();
         mbar_arrive(&bars.o_empty[t]);
       }
+      FWD_T(te1);
+      FWD_ACC(6, te0, te1);
+#ifdef DCPX_FWD_PROFILE
+      ++fprof[8];
+#endif
     }
+#ifdef DCPX_FWD_PROFILE
+    if (blockIdx.x == 0 && (warp == 4 || warp == 8) && lane == 0)
+      printf("[fwd prof] warp %d total %lld steps %lld  s_wait %lld (first of unit %lld)  ld %lld  max %lld  exp %lld  "
+             "st+arrive %lld  units %lld epilogue %lld\n", warp, clock64() - fprof_t0, fprof[5], fprof[0], fprof[7],
+             fprof[1], fprof[2], fprof[3], fprof[4], fprof[8], fprof[6]);
+#endif
   }
   tc_fence_before();
   __syncthreads();
