@@ -227,6 +227,8 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           __syncwarp();
         }
         if (elect_one()) {
+          // a unit without steps (rows that attend nothing) still took a Q buffer
+          if (U.step_count == 0) umma_commit(&bars.q_empty);
           for (int t = 0; t < 2; ++t)
             if (has[t]) umma_commit(&bars.o_full[t]);
         }
