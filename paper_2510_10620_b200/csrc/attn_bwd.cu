@@ -217,12 +217,18 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       constexpr uint32_t id_s = idesc_bf16_f32(128, 64, 0, 0);   // S^T, dP^T: K-major A and B, N = 64 q
       constexpr uint32_t id_g = idesc_bf16_f32(128, 128, 0, 1);  // dV, dK: B = Q / dO MN-major, N = 128 d
       constexpr uint32_t id_q = idesc_bf16_f32(128, 64, 1, 1);   // dQ^T: A = K^T, B = dS^T, both MN-major
-      const uint32_t sk = smem_u32(sK), sv = smem_u32(sV), sds0 = smem_u32(sDS), sst = smem_u32(sStage);
+      // descriptor low words (sdesc_lo): K-major operands (LBO 16) for S^T / dP^T, MN-major
+      // Q / dO (LBO 8192) for dV / dK, MN-major K (LBO 16384) and dS^T (LBO 8192) for dQ^T;
+      // stage / slot / k-slice offsets are added as (byte offset >> 4)
+      const uint32_t k_km = sdesc_lo(smem_u32(sK), 16), v_km = sdesc_lo(smem_u32(sV), 16);
+      const uint32_t st_km = sdesc_lo(smem_u32(sStage), 16), st_mn = sdesc_lo(smem_u32(sStage), 8192);
+      const uint32_t k_mn = sdesc_lo(smem_u32(sK), 16384), ds_mn = sdesc_lo(smem_u32(sDS), 8192);
+      constexpr uint32_t kStageLo = kBwdStageBytes >> 4, kDoLo = 16384 >> 4;
       BWD_PROF_DECL
       // gradient MMAs of step g (stage st, slot b); first = first step of its unit
       auto grads = [&](uint32_t g, bool first, uint32_t it) {
         const uint32_t b = g & 1, st = g % kBwdStages;
-        const uint32_t sq = sst + st * kBwdStageBytes, sdo = sq + 16384, sds = sds0 + b * 16384;
+        const uint32_t q_mn = st_mn + st * kStageLo, do_mn = q_mn + kDoLo, dsb = ds_mn + b * (16384 >> 4);
         BWD_TIMED(2, mbar_wait(&bars.p_ready[b], (g >> 1) & 1));
         tc_fence_after();
         if (first) {
@@ -233,19 +239,16 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           // dV += P^T dO   (A = P^T in TMEM, K = 64 q; B = dO MN-major)
 #pragma unroll
           for (int kk = 0; kk < 4; ++kk)
-            umma_ts(tbase + 256, tbase + 128 * b + kk * 8, sdesc_sw128(sdo + kk * 2048, 8192, 1024), id_g,
-                    (!first || kk > 0) ? 1u : 0u);
+            umma_ts_lo(tbase + 256, tbase + 128 * b + kk * 8, do_mn + kk * 128, id_g, (!first || kk > 0) ? 1u : 0u);
           // dK += dS^T Q   (A = dS^T bf16 in TMEM slot cols [32,64); B = Q MN-major)
 #pragma unroll
           for (int kk = 0; kk < 4; ++kk)
-            umma_ts(tbase + 384, tbase + 128 * b + 32 + kk * 8, sdesc_sw128(sq + kk * 2048, 8192, 1024), id_g,
-                    (!first || kk > 0) ? 1u : 0u);
+            umma_ts_lo(tbase + 384, tbase + 128 * b + 32 + kk * 8, q_mn + kk * 128, id_g, (!first || kk > 0) ? 1u : 0u);
           umma_commit(&bars.q_empty[st]);
           // dQ^T = K^T dS^T (A = K MN-major over d, B = dS^T MN-major over q; K = 128 kv) -> dP^T slot
 #pragma unroll
           for (int kk = 0; kk < 8; ++kk)
-            umma_ss(tbase + 128 * b + 64, sdesc_sw128(sk + kk * 2048, 16384, 1024),
-                    sdesc_sw128(sds + kk * 2048, 8192, 1024), id_q, kk > 0);
+            umma_ss_lo(tbase + 128 * b + 64, k_mn + kk * 128, dsb + kk * 128, id_q, kk > 0);
           umma_commit(&bars.dq_full[b]);
           umma_commit(&bars.ds_free[b]);
         }
@@ -258,7 +261,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         tc_fence_after();
         for (int j = 0; j < U.step_count; ++j, ++g) {
           const uint32_t b = g & 1, st = g % kBwdStages;
-          const uint32_t sq = sst + st * kBwdStageBytes, sdo = sq + 16384;
+          const uint32_t q_km = st_km + st * kStageLo, do_km = q_km + kDoLo;
           BWD_TIMED(0, mbar_wait(&bars.q_full[st], (g / kBwdStages) & 1));
           tc_fence_after();
           // S^T = K Q^T -> slot b cols [0,64). Its previous occupant P^T(g-2) was read by
@@ -266,8 +269,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           if (elect_one()) {
 #pragma unroll
             for (int kk = 0; kk < 8; ++kk)
-              umma_ss(tbase + 128 * b, sdesc_sw128(sk + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024),
-                      sdesc_sw128(sq + (kk >> 2) * 8192 + (kk & 3) * 32, 16, 1024), id_s, kk > 0);
+              umma_ss_lo(tbase + 128 * b, k_km + (kk >> 2) * 1024 + (kk & 3) * 2, q_km + (kk >> 2) * 512 + (kk & 3) * 2,
+                         id_s, kk > 0);
           }
           __syncwarp();
           // dP^T = V dO^T -> slot b cols [64,128), once dQ^T(g-2) has been drained from there
@@ -278,8 +281,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           if (elect_one()) {
 #pragma unroll
             for (int kk = 0; kk < 8; ++kk)
-              umma_ss(tbase + 128 * b + 64, sdesc_sw128(sv + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024),
-                      sdesc_sw128(sdo + (kk >> 2) * 8192 + (kk & 3) * 32, 16, 1024), id_s, kk > 0);
+              umma_ss_lo(tbase + 128 * b + 64, v_km + (kk >> 2) * 1024 + (kk & 3) * 2,
+                         do_km + (kk >> 2) * 512 + (kk & 3) * 2, id_s, kk > 0);
             umma_commit(&bars.s_full[b]);
           }
           __syncwarp();
