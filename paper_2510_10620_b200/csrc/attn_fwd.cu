@@ -151,15 +151,16 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     {
       constexpr uint32_t id_s = idesc_bf16_f32(128, 128, 0, 0);  // Q K^T : both K-major
       constexpr uint32_t id_o = idesc_bf16_f32(128, 128, 0, 1);  // P V   : V is MN-major
-      const uint32_t sq = smem_u32(sQ), sk = smem_u32(sK), sv = smem_u32(sV);
+      // descriptor low words (sdesc_lo); stage / k-slice offsets added as (bytes >> 4)
+      const uint32_t q_lo = sdesc_lo(smem_u32(sQ), 16), k_lo = sdesc_lo(smem_u32(sK), 16);
+      const uint32_t v_lo = sdesc_lo(smem_u32(sV), 16384);
       uint32_t g = 0, it = 0, cnt_p[2] = {0, 0}, cnt_o[2] = {0, 0};
       auto issue_s = [&](int t, int st) {
         if (elect_one()) {
 #pragma unroll
           for (int kk = 0; kk < 8; ++kk) {
-            const uint32_t off = (kk >> 2) * 16384 + (kk & 3) * 32;
-            umma_ss(tbase + 128 * t, sdesc_sw128(sq + t * 32768 + off, 16, 1024),
-                    sdesc_sw128(sk + st * 32768 + off, 16, 1024), id_s, kk > 0);
+            const uint32_t off = (kk >> 2) * 1024 + (kk & 3) * 2;
+            umma_ss_lo(tbase + 128 * t, q_lo + t * 2048 + off, k_lo + st * 2048 + off, id_s, kk > 0);
           }
           umma_commit(&bars.s_full[t]);
         }
@@ -209,9 +210,8 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
             if (elect_one()) {
 #pragma unroll
               for (int kk = 0; kk < 8; ++kk)
-                umma_ts(tbase + 256 + 128 * t, tbase + 128 * t + kk * 8,
-                        sdesc_sw128(sv + st * 32768 + kk * 2048, 16384, 1024), id_o,
-                        (!first[t] || kk > 0) ? 1u : 0u);
+                umma_ts_lo(tbase + 256 + 128 * t, tbase + 128 * t + kk * 8, v_lo + st * 2048 + kk * 128, id_o,
+                           (!first[t] || kk > 0) ? 1u : 0u);
             }
             __syncwarp();
             first[t] = false;
