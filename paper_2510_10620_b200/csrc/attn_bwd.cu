@@ -367,24 +367,26 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           tmem_ld32(slot + 64 + 32 * h, dr);
           tmem_wait_ld();
           uint32_t pk[16], dk[16];
+          const float2 c_s = make_float2(p.scale_log2, p.scale_log2), c_d = make_float2(p.scale, p.scale);
 #pragma unroll
           for (int e4 = 0; e4 < 8; ++e4) {
+            // -LSE * log2(e) and -Delta * scale per q column (delta_kernel stores them so)
             const float4 l4 = lse4[8 * h + e4];
             const float4 d4 = dlt4[8 * h + e4];
-            const float lv[4] = {l4.x, l4.y, l4.z, l4.w};
-            const float dv[4] = {d4.x, d4.y, d4.z, d4.w};
-            float pv[4], sv[4];
+            const float2 nl[2] = {make_float2(l4.x, l4.y), make_float2(l4.z, l4.w)};
+            const float2 nd[2] = {make_float2(d4.x, d4.y), make_float2(d4.z, d4.w)};
 #pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              const int i = 4 * e4 + e;
-              const float pe = fast_exp2(fmaf(__uint_as_float(sr[i]), p.scale_log2, -lv[e]));
-              pv[e] = ((mb[h] >> i) & 1u) ? pe : 0.f;
-              sv[e] = pv[e] * (__uint_as_float(dr[i]) - dv[e]) * p.scale;
+            for (int e2 = 0; e2 < 2; ++e2) {
+              const int i = 4 * e4 + 2 * e2;
+              // P = 2^(s * scale * log2e - LSE * log2e); dS = P * (dP * scale - Delta * scale)
+              const float2 x = ffma2(make_float2(__uint_as_float(sr[i]), __uint_as_float(sr[i + 1])), c_s, nl[e2]);
+              const float2 t = ffma2(make_float2(__uint_as_float(dr[i]), __uint_as_float(dr[i + 1])), c_d, nd[e2]);
+              const float p0 = fast_exp2(x.x), p1 = fast_exp2(x.y);
+              const float2 pv = make_float2(((mb[h] >> i) & 1u) ? p0 : 0.f, ((mb[h] >> (i + 1)) & 1u) ? p1 : 0.f);
+              const float2 sv = fmul2(pv, t);
+              pk[2 * e4 + e2] = pack_bf16(pv.x, pv.y);
+              dk[2 * e4 + e2] = pack_bf16(sv.x, sv.y);
             }
-            pk[2 * e4] = pack_bf16(pv[0], pv[1]);
-            pk[2 * e4 + 1] = pack_bf16(pv[2], pv[3]);
-            dk[2 * e4] = pack_bf16(sv[0], sv[1]);
-            dk[2 * e4 + 1] = pack_bf16(sv[2], sv[3]);
           }
           // P^T / dS^T row j, q columns [32h, 32h+32) as bf16 pairs -> slot cols
           // [16h, 16h+16) / [32+16h, 48+16h) (A operands of dV / dK)

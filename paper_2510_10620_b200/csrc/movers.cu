@@ -141,8 +141,10 @@ __global__ void delta_kernel(const RowJob* __restrict__ jobs, const int32_t* __r
 #pragma unroll
   for (int o = 8; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
   if (r < J.rows && sub == 0) {
-    delta[(int64_t)J.b_row0 + r] = s;
-    lse2[(int64_t)J.b_row0 + r] = lse_arena[(int64_t)J.a_row0 + r] * 1.4426950408889634f;
+    // stored negated and pre-scaled for the backward kernel's packed FMAs:
+    // -Delta * scale and -LSE * log2(e) (scale = 1/sqrt(128))
+    delta[(int64_t)J.b_row0 + r] = -s * 0.08838834764831845f;
+    lse2[(int64_t)J.b_row0 + r] = -lse_arena[(int64_t)J.a_row0 + r] * 1.4426950408889634f;
   }
 }
 

@@ -89,8 +89,8 @@ struct BwdParams {
   const BwdStep* steps;
   const ItemMask* items;
   const int32_t* ranges;
-  const float* lse2;   // LSE * log2(e) per Q-arena row
-  const float* delta;  // rowsum(dO o O) per Q-arena row
+  const float* lse2;   // -LSE * log2(e) per Q-arena row (negated for the packed FMA)
+  const float* delta;  // -rowsum(dO o O) * scale per Q-arena row
   float* dq_acc;       // [Q-arena rows][128] fp32
   float* dkv_acc;      // [KV-arena rows][128] fp32
   int32_t num_units;
