@@ -10,6 +10,7 @@
 #include <cmath>
 #include <cstring>
 #include <map>
+#include <tuple>
 #include <numeric>
 #include <set>
 #include <utility>
@@ -402,7 +403,6 @@ void Executor::compile_device(int d) {
             U.kv_row0 = static_cast<int32_t>(2 * kv_slot * SR + 128 * ks);
             U.n_kv = std::min(128, n_k - 128 * ks);
             U.step_begin = static_cast<int32_t>(bsteps.size());
-            int64_t cur_window = -1;
             auto close = [&]() {
               U.step_count = static_cast<int32_t>(bsteps.size()) - U.step_begin;
               if (U.step_count > 0) {
@@ -412,19 +412,31 @@ void Executor::compile_device(int d) {
               }
               U.step_begin = static_cast<int32_t>(bsteps.size());
             };
+            // (item, q tile) steps of this sub-tile grouped into windows. With
+            // bwd_merge_heads the items of one q block (the GQA group's heads, same tokens)
+            // share their windows, so a unit streams win q tiles of every head: 4x longer
+            // units (fewer K/V reloads and dK/dV epilogues) with the same q-row locality.
+            std::map<std::tuple<int64_t, int64_t, int64_t, int64_t>, std::vector<std::pair<int, int>>> windows;
+            std::vector<std::tuple<int64_t, int64_t, int64_t, int64_t>> window_order;
             for (int idx : idxs) {
               const auto& it = P.items[idx];
               if (it.kv_end - it.kv_begin != n_k) throw Failure(DCPX_ERROR, "kv slot read with two sizes in one instruction");
               const auto& c = icl.at(idx);
-              const int n_q = static_cast<int>(it.q_end - it.q_begin);
               for (int qt = 0; qt < c.n_qb; ++qt) {
+                if (!c.cls_b[qt * c.nks + ks]) continue;
+                const auto key = opt.bwd_merge_heads ? std::make_tuple(int64_t{it.seq}, it.q_begin, it.q_end, int64_t{qt / win})
+                                                     : std::make_tuple(int64_t{idx}, int64_t{0}, int64_t{0}, int64_t{qt / win});
+                auto& w = windows[key];
+                if (w.empty()) window_order.push_back(key);
+                w.emplace_back(idx, qt);
+              }
+            }
+            for (const auto& key : window_order) {
+              for (const auto& [idx, qt] : windows[key]) {
+                const auto& it = P.items[idx];
+                const auto& c = icl.at(idx);
+                const int n_q = static_cast<int>(it.q_end - it.q_begin);
                 const uint32_t cl = c.cls_b[qt * c.nks + ks];
-                if (!cl) continue;
-                const int64_t window = static_cast<int64_t>(idx) * (1 << 20) + qt / win;
-                if (window != cur_window) {
-                  close();
-                  cur_window = window;
-                }
                 BwdStep S{};
                 S.q_row0 = static_cast<int32_t>(it.q_slot * SR + kBwdQRows * qt);
                 S.n_q = std::min(kBwdQRows, n_q - kBwdQRows * qt);
@@ -434,8 +446,8 @@ void Executor::compile_device(int d) {
                 S.cls = cl;
                 bsteps.push_back(S);
               }
+              close();
             }
-            close();
           }
         }
         std::vector<size_t> border(bunits.size());

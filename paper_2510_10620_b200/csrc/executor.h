@@ -136,6 +136,8 @@ struct Options {
   int bwd_order = 2;
   int bwd_window = 16;
   int bwd_window_min_steps = 128;
+  // windows span every item of one q block (the heads of the GQA group) instead of one item
+  int bwd_merge_heads = 1;
 };
 
 class Executor;
