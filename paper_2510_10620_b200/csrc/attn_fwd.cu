@@ -35,6 +35,8 @@ namespace dcpx {
 #define DCPX_SOFT_EXP_PAIRS 0
 #endif
 constexpr int kSoftExpPairs = DCPX_SOFT_EXP_PAIRS;
+// Also measured (after the descriptor-issue change, 6.99 ms): exponent arguments as packed
+// FFMA2 pairs 7.14 ms; plus 2 / 4 of 16 pairs through a packed-FMA soft_exp2: 7.13 / 7.17.
 // Also measured and not kept: row max / row sum as 4 independent chains instead of one
 // FMNMX3 / FADD chain (cfg2 7.51 vs 7.38 ms), and splitting the S load so the first half's
 // max overlaps the second half's tcgen05.ld (much slower: the loaded registers spill).
