@@ -8,9 +8,11 @@
 // steps of the division that touch it (all heads of the GQA group), accumulating dK and
 // dV in TMEM. dQ of each step is reduce-added (fp32, TMA) into the q slot's accumulator.
 //
-// Software pipeline: the MMA issuer runs S^T(g), dP^T(g) one step ahead of the gradient
+// Software pipeline: the MMA issuer runs dP^T(g), S^T(g) one step ahead of the gradient
 // MMAs dV(g-1), dK(g-1), dQ^T(g-1), and two compute warpgroups take alternate steps, so
-// the softmax-gradient math of step g overlaps the tensor work of step g-1.
+// the softmax-gradient math of step g overlaps the tensor work of step g-1. K is also kept
+// in TMEM for the whole unit, so S^T = K Q^T is a TS MMA (only Q read from shared memory:
+// at N = 64 the SS form is shared-memory bound, 48 instead of 32 cycles per K=16 slice).
 //
 // CTA = 512 threads, persistent:
 //   warp 0      TMA producer: Q, dO tiles + LSE/Delta rows per step (3 stages)
@@ -18,13 +20,15 @@
 //   warp 2      TMA producer: K, V per unit
 //   warp 3      idle (register donor)
 //   warps 4-7   compute group 0 (even steps), warps 8-11 compute group 1 (odd steps):
-//               TMEM lane = kv row; P^T (bf16) -> TMEM, dS^T -> smem (SW128). At the end
-//               of a unit group 0 adds dV and group 1 adds dK to the fp32 accumulators.
+//               TMEM lane = kv row; P^T (bf16) -> TMEM, dS^T -> smem (SW128). The group
+//               taking a unit's first step first copies the unit's K tile into TMEM.
 //   warps 12-15 dQ drain: dQ^T (TMEM lane = head dim) -> the step's Q/dO stage buffers
 //               (fp32 [q][d], SW128) -> TMA bulk-tensor reduce-add into the accumulator.
-// TMEM (512 cols): slot b in {0,1} = S^T [128b, 128b+64) (then P^T and dS^T as bf16 in its
-//       two 32-col halves: A operands of dV and dK) | dP^T [128b+64, 128b+128) (reused for
-//       dQ^T); dV [256,384); dK [384,512). dS^T also goes to smem: B operand of dQ^T.
+// TMEM (512 cols): K (bf16 pairs, A operand of S^T) [0,64) | slot b in {0,1} = S^T
+//       [64+64b, 128+64b) (then P^T and dS^T as bf16 in its two 32-col halves: A operands of
+//       dV and dK; then dQ^T) | dP^T [192,256) (single: the compute group frees it as soon
+//       as it has loaded it) | dV [256,384) | dK [384,512). dS^T also goes to smem: B operand
+//       of dQ^T.
 // Masks: for partial tiles each lane builds 32-bit words "q row -> kv rows of my warp"
 // from the q rows' <= 2 attend ranges and transposes them across the warp (5 shuffles),
 // giving every kv-row thread a bitmask over its q columns; the element loop is branch-free.
@@ -39,6 +43,9 @@
 namespace dcpx {
 
 constexpr int kBwdThreads = 512;
+// TMEM columns: K (bf16 pairs, A operand of S^T) | S^T slots 0, 1 (P^T / dS^T, then dQ^T) |
+// dP^T (single) | dV | dK
+constexpr uint32_t kTmK = 0, kTmS = 64, kTmDP = 192, kTmDV = 256, kTmDK = 384;
 constexpr int kBwdStages = 3;
 // K 32K | V 32K | dS^T[2] 32K | stages[3] x (Q 16K | dO 16K) | dQ / dK / dV staging 32K |
 // LSE[3] 1K | Delta[3] 1K | barriers
@@ -52,7 +59,9 @@ struct BwdBarriers {
   uint64_t q_full[kBwdStages], q_empty[kBwdStages];
   uint64_t s_full[2], p_ready[2], dq_full[2], dq_empty[2], ds_free[2];
   uint64_t acc_full, acc_empty;
+  uint64_t ktm_full, dp_free;
   uint32_t tmem_base;
+  uint32_t kv_seq;  // units whose K / V the MMA warp has seen land (monotonic)
 };
 
 // fp32 vector reduce-add into global memory (accumulators are shared with other CTAs
@@ -146,6 +155,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     }
     mbar_init(&bars.acc_full, 1);
     mbar_init(&bars.acc_empty, 128);  // drain warpgroup: dK / dV read out of TMEM
+    mbar_init(&bars.ktm_full, 128);   // compute group of the unit's first step: K in TMEM
+    mbar_init(&bars.dp_free, 128);    // compute group of step g: dP^T(g) loaded
+    bars.kv_seq = 0;
     fence_barrier_init();
     tma_prefetch_desc(&tm_q);
     tma_prefetch_desc(&tm_do);
@@ -239,16 +251,17 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           // dV += P^T dO   (A = P^T in TMEM, K = 64 q; B = dO MN-major)
 #pragma unroll
           for (int kk = 0; kk < 4; ++kk)
-            umma_ts_lo(tbase + 256, tbase + 128 * b + kk * 8, do_mn + kk * 128, id_g, (!first || kk > 0) ? 1u : 0u);
+            umma_ts_lo(tbase + kTmDV, tbase + kTmS + 64 * b + kk * 8, do_mn + kk * 128, id_g, (!first || kk > 0) ? 1u : 0u);
           // dK += dS^T Q   (A = dS^T bf16 in TMEM slot cols [32,64); B = Q MN-major)
 #pragma unroll
           for (int kk = 0; kk < 4; ++kk)
-            umma_ts_lo(tbase + 384, tbase + 128 * b + 32 + kk * 8, q_mn + kk * 128, id_g, (!first || kk > 0) ? 1u : 0u);
+            umma_ts_lo(tbase + kTmDK, tbase + kTmS + 64 * b + 32 + kk * 8, q_mn + kk * 128, id_g,
+                       (!first || kk > 0) ? 1u : 0u);
           umma_commit(&bars.q_empty[st]);
           // dQ^T = K^T dS^T (A = K MN-major over d, B = dS^T MN-major over q; K = 128 kv) -> dP^T slot
 #pragma unroll
           for (int kk = 0; kk < 8; ++kk)
-            umma_ss_lo(tbase + 128 * b + 64, k_mn + kk * 128, dsb + kk * 128, id_q, kk > 0);
+            umma_ss_lo(tbase + kTmS + 64 * b, k_mn + kk * 128, dsb + kk * 128, id_q, kk > 0);
           umma_commit(&bars.dq_full[b]);
           umma_commit(&bars.ds_free[b]);
         }
@@ -259,30 +272,39 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         const BwdUnit U = p.units[u];
         BWD_TIMED(4, mbar_wait(&bars.kv_full, it & 1));
         tc_fence_after();
+        if (lane == 0) st_release_cta(&bars.kv_seq, it + 1);  // the K writer may copy K
         for (int j = 0; j < U.step_count; ++j, ++g) {
           const uint32_t b = g & 1, st = g % kBwdStages;
           const uint32_t q_km = st_km + st * kStageLo, do_km = q_km + kDoLo;
           BWD_TIMED(0, mbar_wait(&bars.q_full[st], (g / kBwdStages) & 1));
           tc_fence_after();
-          // S^T = K Q^T -> slot b cols [0,64). Its previous occupant P^T(g-2) was read by
-          // dV(g-2), issued earlier on this thread.
-          if (elect_one()) {
-#pragma unroll
-            for (int kk = 0; kk < 8; ++kk)
-              umma_ss_lo(tbase + 128 * b, k_km + (kk >> 2) * 1024 + (kk & 3) * 2, q_km + (kk >> 2) * 512 + (kk & 3) * 2,
-                         id_s, kk > 0);
-          }
-          __syncwarp();
-          // dP^T = V dO^T -> slot b cols [64,128), once dQ^T(g-2) has been drained from there
-          if (g >= 2) {
-            BWD_TIMED(1, mbar_wait(&bars.dq_empty[b], ((g >> 1) - 1) & 1));
+          // dP^T = V dO^T -> the dP^T columns, once the compute group of step g-1 has loaded
+          // its dP^T (issued first: the drain of dQ^T(g-2) out of slot b overlaps it)
+          if (g >= 1) {
+            BWD_TIMED(5, mbar_wait(&bars.dp_free, (g - 1) & 1));
             tc_fence_after();
           }
           if (elect_one()) {
 #pragma unroll
             for (int kk = 0; kk < 8; ++kk)
-              umma_ss_lo(tbase + 128 * b + 64, v_km + (kk >> 2) * 1024 + (kk & 3) * 2,
-                         do_km + (kk >> 2) * 512 + (kk & 3) * 2, id_s, kk > 0);
+              umma_ss_lo(tbase + kTmDP, v_km + (kk >> 2) * 1024 + (kk & 3) * 2, do_km + (kk >> 2) * 512 + (kk & 3) * 2,
+                         id_s, kk > 0);
+          }
+          __syncwarp();
+          // S^T = K Q^T (A = K in TMEM) -> slot b, once dQ^T(g-2) has been drained from it
+          if (g >= 2) {
+            BWD_TIMED(1, mbar_wait(&bars.dq_empty[b], ((g >> 1) - 1) & 1));
+            tc_fence_after();
+          }
+          if (j == 0) {
+            BWD_TIMED(4, mbar_wait(&bars.ktm_full, it & 1));
+            tc_fence_after();
+          }
+          if (elect_one()) {
+#pragma unroll
+            for (int kk = 0; kk < 8; ++kk)
+              umma_ts_lo(tbase + kTmS + 64 * b, tbase + kTmK + kk * 8, q_km + (kk >> 2) * 512 + (kk & 3) * 2, id_s,
+                         kk > 0);
             umma_commit(&bars.s_full[b]);
           }
           __syncwarp();
@@ -295,7 +317,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         }
         __syncwarp();
       }
-      if (lane == 0) BWD_PROF_PRINT("mma", "q_full", "dq_empty", "p_ready", "acc_empty", "kv_full", "-");
+      if (lane == 0) BWD_PROF_PRINT("mma", "q_full", "dq_empty", "p_ready", "acc_empty", "kv+ktm_full", "dp_free");
     }
   } else if (warp >= 4 && warp < 12) {
     // ------------------------------------------------------------ compute warpgroups
@@ -312,6 +334,33 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       const bool kv_valid = j < U.n_kv;
       // descriptors of my next step are loaded a step ahead so their latency hides
       int s = (int)((grp - g) & 1);
+      if (s == 0) {
+        // the unit's first step is mine: copy its K tile (two SW128 halves of 64 d) into TMEM
+        // cols [0,64), lane = kv row. The previous unit's S^T MMAs have completed (K / V of
+        // this unit were loaded after the MMA's commit at the end of that unit). A group can
+        // run units ahead (units without a step of its parity), so it waits for the MMA
+        // warp's absolute unit count instead of a kv_full phase parity, which could alias.
+        BWD_MARK(t_kv);
+        while (ld_acquire_cta(&bars.kv_seq) < it + 1) __nanosleep(20);
+        BWD_ADD(2, t_kv);
+        const uint8_t* krow = sK + j * 128;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          uint32_t kr[32];
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            const uint4 v4 = *reinterpret_cast<const uint4*>(krow + h * 16384 + ((c ^ (j & 7)) << 4));
+            kr[4 * c] = v4.x;
+            kr[4 * c + 1] = v4.y;
+            kr[4 * c + 2] = v4.z;
+            kr[4 * c + 3] = v4.w;
+          }
+          tmem_st32(lane_addr + kTmK + 32 * h, kr);
+        }
+        tmem_wait_st();
+        tc_fence_before();
+        mbar_arrive(&bars.ktm_full);
+      }
       BwdStep s_next{};
       ItemMask m_next{};
       if (s < U.step_count) {
@@ -354,18 +403,20 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         BWD_MARK(t_math);
         const float4* lse4 = reinterpret_cast<const float4*>(sLSE + st * 64);
         const float4* dlt4 = reinterpret_cast<const float4*>(sDelta + st * 64);
-        const uint32_t slot = lane_addr + 128 * b;
-        uint32_t srr[2][32];
-        tmem_ld32(slot, srr[0]);
-        tmem_ld32(slot + 32, srr[1]);
+        const uint32_t slot = lane_addr + kTmS + 64 * b;
+        // all of dP^T(gs) first, so the MMA may overwrite it with dP^T(gs+1) right away;
+        // S^T in halves (half 1 is loaded before half 0's dS^T overwrites its columns)
+        uint32_t sr[32], drr[2][32];
+        tmem_ld32(lane_addr + kTmDP, drr[0]);
+        tmem_ld32(lane_addr + kTmDP + 32, drr[1]);
+        tmem_ld32(slot, sr);
         tmem_wait_ld();
+        tc_fence_before();
+        mbar_arrive(&bars.dp_free);
         uint8_t* row = my_row0 + b * 16384;
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
-          const uint32_t* sr = srr[h];
-          uint32_t dr[32];
-          tmem_ld32(slot + 64 + 32 * h, dr);
-          tmem_wait_ld();
+          const uint32_t* dr = drr[h];
           uint32_t pk[16], dk[16];
           const float2 c_s = make_float2(p.scale_log2, p.scale_log2), c_d = make_float2(p.scale, p.scale);
 #pragma unroll
@@ -388,6 +439,10 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
               dk[2 * e4 + e2] = pack_bf16(sv.x, sv.y);
             }
           }
+          if (h == 0) {
+            tmem_ld32(slot + 32, sr);
+            tmem_wait_ld();
+          }
           // P^T / dS^T row j, q columns [32h, 32h+32) as bf16 pairs -> slot cols
           // [16h, 16h+16) / [32+16h, 48+16h) (A operands of dV / dK)
           tmem_st16(slot + 16 * h, pk);
@@ -408,10 +463,10 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       }
       g += U.step_count;
     }
-    if (lane == 0 && wq == 0) BWD_PROF_PRINT(grp ? "compute1" : "compute0", "s_full", "ds_free", "-", "mask", "math", "-");
+    if (lane == 0 && wq == 0) BWD_PROF_PRINT(grp ? "compute1" : "compute0", "s_full", "ds_free", "kv_seq", "mask", "math", "-");
   } else if (warp >= 12) {
     // ------------------------------------------------------------ drain warpgroup
-    // dQ^T of step g sits in slot g&1 cols [64,128) with TMEM lane = head dim d. Thread d
+    // dQ^T of step g sits in S^T slot g&1 with TMEM lane = head dim d. Thread d
     // writes column d of four [64 q][32 d] fp32 chunks (128B-swizzled; chunk k = d / 32)
     // into the 32 KiB staging area, then one lane reduce-adds them into the dQ accumulator.
     // At the end of a unit the same warps move dV and dK out of TMEM (TMEM lane = kv row)
@@ -432,8 +487,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         BWD_TIMED(0, mbar_wait(&bars.dq_full[b], (g >> 1) & 1));
         tc_fence_after();
         uint32_t v[2][32];
-        tmem_ld32(lane_addr + 128 * b + 64, v[0]);
-        tmem_ld32(lane_addr + 128 * b + 96, v[1]);
+        tmem_ld32(lane_addr + kTmS + 64 * b, v[0]);
+        tmem_ld32(lane_addr + kTmS + 64 * b + 32, v[1]);
         tmem_wait_ld();
         tc_fence_before();
         mbar_arrive(&bars.dq_empty[b]);
@@ -466,7 +521,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       for (int c = 0; c < 8; ++c) {
         uint32_t r[32];
         BWD_MARK(t_ld);
-        tmem_ld32(lane_addr + 256 + 32 * c, r);
+        tmem_ld32(lane_addr + kTmDV + 32 * c, r);
         tmem_wait_ld();
         BWD_ADD(1, t_ld);
         if (c == 7) {
