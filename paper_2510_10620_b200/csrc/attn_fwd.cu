@@ -261,11 +261,6 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       const int64_t orow = (int64_t)U.out_row0 + 128 * t + r;
       __nv_bfloat16* out = p.o_arena + orow * kHeadDim;
       const bool merge = (U.flags & 1) != 0;
-      if (merge && row_valid) {  // the epilogue's merge operands: to L2 while the steps run
-        prefetch_l2(out);
-        prefetch_l2(out + 64);
-        prefetch_l2(p.lse_arena + orow);
-      }
       float m_used = -CUDART_INF_F;  // running max, log2 domain (lazily updated)
       float l = 0.f;
       bool has = false;
@@ -372,7 +367,8 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       }
       FWD_T(te0);
       // ---- epilogue: O / l, LSE, optional merge with the destination's current value.
-      // The merge operands were prefetched to L2 at the start of the unit.
+      // (Prefetching the merge operands to L2 at the start of the unit measured neutral and
+      // cost register spills, so they are read here.)
       float lse_prev = -CUDART_INF_F;
       if (merge && row_valid) lse_prev = p.lse_arena[orow];
       const float lse_new = l > 0.f ? (m_used + __log2f(l)) * 0.69314718055994531f : -CUDART_INF_F;
