@@ -26,6 +26,15 @@ def cfg1_batch():
     return PL.Batch.from_specs(CFG1, 8, 2, 128)
 
 
+# configs[4]: long-tail stress, one 512K causal sequence plus many short ones (48 sequences of
+# 0.5K-4K tokens, 110,592 tokens): 634,880 tokens in one batch
+CFG5 = [PL.SeqSpec(524288)] + [PL.SeqSpec(1024 * (1 + i % 4) - 256 * (i % 3)) for i in range(48)]
+
+
+def cfg5_batch():
+    return PL.Batch.from_specs(CFG5, 32, 8, 128)
+
+
 def synth(mask, max_len, budget, index):
     def f():
         b, _ = PL.Batch.from_synth(mask, max_len, budget, index, 32, 8, seed=42)
@@ -63,6 +72,10 @@ CONFIGS = {
     "cfg4_cb_B1024_R1": (synth("causal_blockwise", 131072, 131072, 0), 1, 1024, {}),
     "cfg4_cb_B2048_R1": (synth("causal_blockwise", 131072, 131072, 0), 1, 2048, {}),
     "cfg4_sq_B2048_R1": (synth("shared_question", 131072, 131072, 0), 1, 2048, {}),
+    # configs[4]: long-tail stress (512K + short tail), causal, block 4096
+    "cfg5_R1": (cfg5_batch, 1, 4096, {}),
+    "cfg5_R4": (cfg5_batch, 4, 4096, {}),
+    "cfg5_R8": (cfg5_batch, 8, 4096, {}),
 }
 
 
