@@ -192,6 +192,7 @@ def main():
         "cfg4_cb_B2048": ("causal-blockwise (256, 2, 1, 1), 128K-token batch", 2048),
         "cfg4_sq_B2048": ("shared-question (4 answers x 20 %), 128K-token batch", 2048),
         "cfg5": ("causal long-tail stress: one 512K-token sequence + 48 short seqs (634,880 tokens)", 4096),
+        "cfg5_B8192": ("causal long-tail stress: one 512K-token sequence + 48 short seqs (634,880 tokens)", 8192),
     }
     desc, block = workloads.get(args.config, (args.config, None))
     config = {"workload": f"{args.config}: 8B-GPT attention layer (32 q / 8 kv heads, d 128), {desc}, "

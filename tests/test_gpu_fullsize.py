@@ -4,7 +4,7 @@ Forward: every config's plan against dense FP64 masked attention (tests/oracle.h
 semantics) on sampled (token, head) rows, computed on the GPU from the same bf16 inputs;
 planned bytes and FLOPs bit-exact (CommVolume, BlockGraph::total_flops).
 Backward (no reference): plan invariance at full size -- the same inputs through the
-1-device and the 4-device plan of config 3 give the same O / LSE / dQ / dK / dV (the
+1-device and the 4-device plan of configs 3 and 5 give the same O / LSE / dQ / dK / dV (the
 reference tests placement independence of the forward the same way,
 tests/test_simexec.cpp:210-222). Plan devices are spread over the GPUs present."""
 import os
@@ -76,7 +76,7 @@ def _run(bundle, q, k, v, d_o=None):
 
 
 @pytest.mark.parametrize("name", ["cfg1_R2", "cfg2_R1", "cfg3_R4", "cfg4_cb_B512_R8", "cfg4_cb_B1024_R8",
-                                  "cfg4_cb_B2048_R8", "cfg4_sq_B2048_R8"])
+                                  "cfg4_cb_B2048_R8", "cfg4_sq_B2048_R8", "cfg5_R1", "cfg5_B8192_R4"])
 def test_fullsize_forward_sampled_rows(name):
     from make_plans import load
     bundle = load(name)
@@ -96,9 +96,10 @@ def test_fullsize_forward_sampled_rows(name):
     assert rep["total_flops"] == int(bundle.total_flops), name
 
 
-def test_fullsize_backward_plan_invariance():
+@pytest.mark.parametrize("cfg", ["cfg3", "cfg5_B8192"])
+def test_fullsize_backward_plan_invariance(cfg):
     from make_plans import load
-    b1, b4 = load("cfg3_R1"), load("cfg3_R4")
+    b1, b4 = load(f"{cfg}_R1"), load(f"{cfg}_R4")
     assert b1.total_tokens == b4.total_tokens and int(b1.total_flops) == int(b4.total_flops)
     q, k, v, d_o = _inputs(b1, seed=9)
     o1, l1, _, g1 = _run(b1, q, k, v, d_o)

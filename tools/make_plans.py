@@ -72,10 +72,13 @@ CONFIGS = {
     "cfg4_cb_B1024_R1": (synth("causal_blockwise", 131072, 131072, 0), 1, 1024, {}),
     "cfg4_cb_B2048_R1": (synth("causal_blockwise", 131072, 131072, 0), 1, 2048, {}),
     "cfg4_sq_B2048_R1": (synth("shared_question", 131072, 131072, 0), 1, 2048, {}),
-    # configs[4]: long-tail stress (512K + short tail), causal, block 4096
+    # configs[4]: long-tail stress (512K + short tail), causal. Block 4096 plans in 40 s for
+    # one device but did not finish within 20 min for 4 or 8 devices (265,728 comp blocks),
+    # so the multi-device plans use block 8192 (68,096 comp blocks; R 4 plans in ~6 min).
     "cfg5_R1": (cfg5_batch, 1, 4096, {}),
-    "cfg5_R4": (cfg5_batch, 4, 4096, {}),
-    "cfg5_R8": (cfg5_batch, 8, 4096, {}),
+    "cfg5_B8192_R1": (cfg5_batch, 1, 8192, {}),
+    "cfg5_B8192_R4": (cfg5_batch, 4, 8192, {}),
+    "cfg5_B8192_R8": (cfg5_batch, 8, 8192, {}),
 }
 
 
