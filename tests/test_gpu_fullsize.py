@@ -54,6 +54,18 @@ def _dense_rows(bundle, q, k, v, toks, heads):
     return np.array(outs), np.array(lses)
 
 
+def _rel_dev(x, ref) -> float:
+    """max |x - ref| / max |ref| on the device, chunked (full-size tensors are ~10 GB in fp32)."""
+    num, den = 0.0, 0.0
+    xf, rf = x.reshape(-1), ref.reshape(-1)
+    step = 1 << 28
+    for i in range(0, xf.numel(), step):
+        a, b = xf[i:i + step].float(), rf[i:i + step].float()
+        num = max(num, float((a - b).abs().max()))
+        den = max(den, float(b.abs().max()))
+    return num / (den if den > 0 else 1.0)
+
+
 def _run(bundle, q, k, v, d_o=None):
     import torch
 
@@ -105,8 +117,10 @@ def test_fullsize_backward_plan_invariance(cfg):
     o1, l1, _, g1 = _run(b1, q, k, v, d_o)
     o4, l4, r4, g4 = _run(b4, q, k, v, d_o)
     assert r4["total_bytes"] == int(b4.volume[0])
-    assert rel_err(o4.float().cpu().numpy(), o1.float().cpu().numpy()) <= 1e-2
-    fin = np.isfinite(l1.cpu().numpy())
-    assert np.abs(l4.cpu().numpy()[fin] - l1.cpu().numpy()[fin]).max() <= LSE_TOL
+    assert _rel_dev(o4, o1) <= 1e-2
+    import torch
+    fin = torch.isfinite(l1)
+    assert torch.equal(torch.isfinite(l4), fin)
+    assert float((l4[fin] - l1[fin]).abs().max()) <= LSE_TOL
     for a, b in zip(g4, g1):
-        assert rel_err(a.float().cpu().numpy(), b.float().cpu().numpy()) <= 1e-2
+        assert _rel_dev(a, b) <= 1e-2
