@@ -20,6 +20,12 @@ REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, os.path.join(REPO, "tools"))
 
 
+# The 635K-token long-tail batch (cfg5) takes 2-4 min per test (host-side prepare of
+# 68K-266K comp blocks, 10 GB tensors): run with DCPX_LONG_TESTS=1 (results of the last run
+# in profiles/r1_cfg5_tests.log).
+LONG = pytest.mark.skipif(not os.environ.get("DCPX_LONG_TESTS"), reason="long test: set DCPX_LONG_TESTS=1")
+
+
 def _ngpu():
     import torch
     return torch.cuda.device_count()
@@ -88,7 +94,9 @@ def _run(bundle, q, k, v, d_o=None):
 
 
 @pytest.mark.parametrize("name", ["cfg1_R2", "cfg2_R1", "cfg3_R4", "cfg4_cb_B512_R8", "cfg4_cb_B1024_R8",
-                                  "cfg4_cb_B2048_R8", "cfg4_sq_B2048_R8", "cfg5_R1", "cfg5_B8192_R4"])
+                                  "cfg4_cb_B2048_R8", "cfg4_sq_B2048_R8",
+                                  pytest.param("cfg5_R1", marks=LONG),
+                                  pytest.param("cfg5_B8192_R4", marks=LONG)])
 def test_fullsize_forward_sampled_rows(name):
     from make_plans import load
     bundle = load(name)
@@ -108,7 +116,7 @@ def test_fullsize_forward_sampled_rows(name):
     assert rep["total_flops"] == int(bundle.total_flops), name
 
 
-@pytest.mark.parametrize("cfg", ["cfg3", "cfg5_B8192"])
+@pytest.mark.parametrize("cfg", ["cfg3", pytest.param("cfg5_B8192", marks=LONG)])
 def test_fullsize_backward_plan_invariance(cfg):
     from make_plans import load
     b1, b4 = load(f"{cfg}_R1"), load(f"{cfg}_R4")
