@@ -51,6 +51,15 @@ constexpr int kSoftExpPairs = DCPX_SOFT_EXP_PAIRS;
 #define FWD_ACC(i, a, b)
 #endif
 
+// P handed to the PV MMA in two halves (K-slices 0-3 after the first 64 columns are stored),
+// so the first half of PV overlaps the second half of the exponentials. Measured (min of 10,
+// alternating A/B on one B200): cfg2 7.05 -> 7.15 ms, cfg3 8.04 -> 8.00, shared-question
+// 33.8 -> 34.5 ms (parity green), so it is off by default.
+#ifndef DCPX_FWD_SPLIT_P
+#define DCPX_FWD_SPLIT_P 0
+#endif
+constexpr bool kSplitP = DCPX_FWD_SPLIT_P != 0;
+
 constexpr int kFwdThreads = 384;
 constexpr int kFwdSmem = 6 * 32768 + 1024;  // Q0 Q1 K[2] V[2] + alignment slack
 constexpr float kRescaleThreshold = 8.0f;   // log2 units: lazy O rescale (factor 256)
@@ -58,7 +67,7 @@ constexpr float kRescaleThreshold = 8.0f;   // log2 units: lazy O rescale (facto
 struct FwdBarriers {
   uint64_t q_full, q_empty;
   uint64_t k_full[2], v_full[2], kv_empty[2];
-  uint64_t s_full[2], p_ready[2], o_full[2], o_empty[2];
+  uint64_t s_full[2], p_half[2], p_ready[2], o_full[2], o_empty[2];
   uint32_t tmem_base;
 };
 
@@ -98,6 +107,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       mbar_init(&bars.v_full[i], 1);
       mbar_init(&bars.kv_empty[i], 1);
       mbar_init(&bars.s_full[i], 1);
+      mbar_init(&bars.p_half[i], 128);
       mbar_init(&bars.p_ready[i], 128);
       mbar_init(&bars.o_full[i], 1);
       mbar_init(&bars.o_empty[i], 128);
@@ -202,8 +212,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
 #pragma unroll
           for (int t = 0; t < 2; ++t) {
             if (!cls_of(c, t)) continue;
-            mbar_wait(&bars.p_ready[t], cnt_p[t] & 1);
-            ++cnt_p[t];
+            mbar_wait(kSplitP ? &bars.p_half[t] : &bars.p_ready[t], cnt_p[t] & 1);
             tc_fence_after();
             if (first[t]) {
               mbar_wait(&bars.o_empty[t], (cnt_o[t] & 1) ^ 1);
@@ -211,11 +220,22 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
             }
             if (elect_one()) {
 #pragma unroll
-              for (int kk = 0; kk < 8; ++kk)
+              for (int kk = 0; kk < (kSplitP ? 4 : 8); ++kk)
                 umma_ts_lo(tbase + 256 + 128 * t, tbase + 128 * t + kk * 8, v_lo + st * 2048 + kk * 128, id_o,
                            (!first[t] || kk > 0) ? 1u : 0u);
             }
             __syncwarp();
+            if (kSplitP) {
+              mbar_wait(&bars.p_ready[t], cnt_p[t] & 1);
+              tc_fence_after();
+              if (elect_one()) {
+#pragma unroll
+                for (int kk = 4; kk < 8; ++kk)
+                  umma_ts_lo(tbase + 256 + 128 * t, tbase + 128 * t + kk * 8, v_lo + st * 2048 + kk * 128, id_o, 1u);
+              }
+              __syncwarp();
+            }
+            ++cnt_p[t];
             first[t] = false;
             if (j + 1 < U.step_count && cls_of(steps[j + 1].cls, t)) {
               const uint32_t g2 = g + 1;
@@ -350,6 +370,11 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
             pk[e] = pack_bf16(p0, p1);
           }
           tmem_st16(lane_addr + s_col + (c >> 1), pk);
+          if (kSplitP && c == 32) {  // P columns [0, 32) (K-slices 0-3) are in TMEM
+            tmem_wait_st();
+            tc_fence_before();
+            mbar_arrive(&bars.p_half[t]);
+          }
         }
         l += sum;
         FWD_T(t4);
