@@ -225,8 +225,10 @@ cudaEvent_t Executor::event(int d) {
 
 // Persistent attention grids leave `sm_reserve` SMs free when the plan communicates, so
 // transfer kernels on the (high-priority) comm stream run concurrently with compute.
+// Default 4 (profiles/r1_sm_reserve_sweep.log, cfg2 per-rank): N = 4 2910 vs 2817 TFLOP/s
+// with 8, N = 2 1624-1653 vs 1601-1609; one cfg3 N = 4 sample was 2 % slower (2482 vs 2531).
 int Executor::attn_grid(int d, int grid) const {
-  const int reserve = opt.sm_reserve >= 0 ? opt.sm_reserve : (R_ > 1 ? 8 : 0);
+  const int reserve = opt.sm_reserve >= 0 ? opt.sm_reserve : (R_ > 1 ? 4 : 0);
   const int cap = std::max(1, num_sms(dev_[d].ordinal) - reserve);
   return std::min(grid, cap);
 }
