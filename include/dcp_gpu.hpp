@@ -187,12 +187,22 @@ inline SimResult run(const std::vector<ExecutionPlan>& plans, const BlockGraph& 
   detail::Flat f;
   detail::flatten(plans, g, f);
   dcpx_ctx* ctx = nullptr;
-  detail::throw_status(dcpx_create(R, cuda_ordinals.data(), DCPX_TRANSPORT_LOCAL, &ctx), dcpx_last_error(nullptr));
   struct Guard {
     dcpx_ctx* c;
     ~Guard() { dcpx_destroy(c); }
-  } guard{ctx};
-  detail::throw_status(dcpx_prepare(ctx, R, f.views.data(), &f.graph, &f.masks), dcpx_last_error(ctx));
+  } guard{nullptr};
+  if (options.numeric) {
+    detail::throw_status(dcpx_create(R, cuda_ordinals.data(), DCPX_TRANSPORT_LOCAL, &ctx), dcpx_last_error(nullptr));
+    guard.c = ctx;
+    detail::throw_status(dcpx_prepare(ctx, R, f.views.data(), &f.graph, &f.masks), dcpx_last_error(ctx));
+  } else {
+    // cost-only run (SimOptions::numeric false): no GPU work, so no context; the plans still
+    // get the reference's checks (verify_plans and the lockstep deadlock / tag replay), and
+    // any head_dim / element size is accepted as the reference's run() accepts it
+    char err[1024];
+    const dcpx_status st = dcpx_check_plans(R, f.views.data(), &f.graph, &f.masks, err, sizeof(err));
+    detail::throw_status(st, err);
+  }
 
   const auto& b = g.batch;
   const int H = b.heads, G = b.kv_groups, D = b.head_dim;
@@ -217,6 +227,7 @@ inline SimResult run(const std::vector<ExecutionPlan>& plans, const BlockGraph& 
     }
     detail::throw_status(dcpx_load_inputs_host(ctx, q.data(), k.data(), v.data()), dcpx_last_error(ctx));
     detail::throw_status(dcpx_forward_host(ctx, o.data(), nullptr, &rep), dcpx_last_error(ctx));
+    detail::throw_status(dcpx_synchronize(ctx), dcpx_last_error(ctx));  // host outputs are asynchronous
     result.outputs.o.resize(b.sequences.size());
     for (size_t s = 0; s < b.sequences.size(); ++s) {
       const int L = static_cast<int>(b.sequences[s].length);

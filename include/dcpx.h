@@ -159,13 +159,27 @@ typedef struct {
   int32_t attn_launches;             /* attention kernel (K1 / K1b) launches of the last call */
   double attn_ms;                    /* max over devices of the summed device time of those launches */
   double attn_ms_sum;                /* the same summed over devices (GPU-time spent in the kernel) */
+  /* bytes the transfers of the call actually move per device (wire_bytes split by sender /
+   * receiver): forward O transfers carry the fp32 LSE (4 B/row); backward Q fetches carry
+   * Q + dO + fp32 LSE and Delta (8 B/row); gradient returns are fp32 (2x the planned bytes) */
+  uint64_t wire_per_device_send[64];
+  uint64_t wire_per_device_recv[64];
+  int32_t units;                     /* attention work units of the call (K1 FwdUnit / K1b BwdUnit) */
+  int32_t windowed;                  /* backward: attention instructions with q-windowed units */
 } dcpx_report;
 
 typedef struct dcpx_ctx dcpx_ctx;
 
 /* One process executes all `ndev` plan devices; plan device d runs on CUDA device
- * cuda_ordinals[d] (several plan devices may share one GPU). Transfers are
- * device-to-device copies on per-device comm streams. transport must be LOCAL. */
+ * cuda_ordinals[d] (several plan devices may share one GPU). Transfers run on per-device
+ * comm streams: LOCAL = copy kernels reading the sender's slots over NVLink peer memory;
+ * NCCL = ncclSend/ncclRecv groups (needs one distinct GPU per plan device).
+ *
+ * Stream contract: every load_inputs / forward / backward call is ordered after the work
+ * already enqueued on the caller's stream of each plan device (by default the legacy
+ * default stream; see dcpx_set_streams), and that stream waits for the call's device work,
+ * so device inputs produced and outputs consumed on the caller's stream need no host
+ * synchronisation. Host buffers (the _host calls) are valid after dcpx_synchronize. */
 dcpx_status dcpx_create(int ndev, const int* cuda_ordinals, dcpx_transport transport,
                         dcpx_ctx** out);
 
@@ -218,7 +232,7 @@ dcpx_status dcpx_backward(dcpx_ctx* ctx, const void* d_o, void* dq, void* dk, vo
 /* Host-buffer backward, asynchronous like dcpx_load_inputs_host: dq/dk/dv are valid after
  * the next dcpx_synchronize (uploads and downloads run on their own streams, so
  * consecutive steps overlap their PCIe traffic with compute). dcpx_forward_host is
- * synchronous (o_out/lse_out valid on return). */
+ * asynchronous the same way: o_out / lse_out are valid after dcpx_synchronize. */
 dcpx_status dcpx_backward_host(dcpx_ctx* ctx, const void* d_o, void* dq, void* dk, void* dv,
                                dcpx_report* rep);
 
@@ -237,10 +251,24 @@ dcpx_status dcpx_backward_dev(dcpx_ctx* ctx, const void* const* d_o, void* const
 /* Synchronises all streams of the context. */
 dcpx_status dcpx_synchronize(dcpx_ctx* ctx);
 
+/* The caller's CUDA stream (cudaStream_t) on each of the n = ndev plan devices (per-rank
+ * mode: n = world, only entry [rank] is used); NULL entries select the legacy default
+ * stream. Applies to the following calls (stream contract above). */
+dcpx_status dcpx_set_streams(dcpx_ctx* ctx, int n, void* const* streams);
+
+/* Host-only plan check (no context, no GPU): ingests the views and runs the static checks
+ * of verify_plans (plan.hpp:388-475) plus the lockstep replay of run() (deadlock and tag
+ * errors, simexec.hpp:375-397). Returns the status the executor's prepare would raise for
+ * these plans; err (may be NULL) receives the message, NUL-terminated, truncated to cap. */
+dcpx_status dcpx_check_plans(int nplans, const dcpx_plan_view* plans, const dcpx_graph_view* graph,
+                             const dcpx_mask_view* masks, char* err, int64_t cap);
+
 /* Test / introspection hooks (not part of the reference surface). */
 /* Device pointers of the slot arenas of plan device `dev`: kind 0 Q, 1 KV, 2 O, 3 LSE. */
 dcpx_status dcpx_debug_arena(dcpx_ctx* ctx, int dev, int kind, void** ptr, int64_t* slot_rows);
-/* Executor options: "fuse_reductions", "remap_copies", "timing", "kernel_timing", "trace". */
+/* Executor options: "fuse_reductions", "remap_copies", "timing" (report device_ms; blocks
+ * the host at the end of each call; default off), "kernel_timing", "trace", "sm_transfers",
+ * "sm_reserve", "bwd_order", "bwd_window", "bwd_window_min_steps", "bwd_merge_heads". */
 dcpx_status dcpx_set_option(dcpx_ctx* ctx, const char* key, int64_t value);
 
 /* Op trace of the last forward/backward (option "trace"): rows of 7 doubles

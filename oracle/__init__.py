@@ -238,3 +238,28 @@ def ref_time_items(nq, nk, row_off, rows, D, threads):
     if rc:
         raise RuntimeError(ref().dcpr_last_error().decode())
     return sec.value
+
+
+def ref_run_items(items, D, threads):
+    """Reference exec_attention (simexec.hpp:33-76) on `items`, a list of dicts with
+    nq, nk, rows [nq, 4] (kv-tile-relative) and q [nq, D], k, v [nk, D] float64 inputs, on
+    `threads` host threads. Returns (outs list of [nq, D], lses list of [nq], seconds)."""
+    n = len(items)
+    nq = np.array([it["q"].shape[0] for it in items], np.int32)
+    nk = np.array([it["k"].shape[0] for it in items], np.int32)
+    row_off = np.concatenate([[0], np.cumsum(nq)[:-1]]).astype(np.int64)
+    k_off = np.concatenate([[0], np.cumsum(nk)[:-1]]).astype(np.int64)
+    rows = np.ascontiguousarray(np.concatenate([it["rows"] for it in items]), np.int32)
+    qa = _f64(np.concatenate([it["q"] for it in items]))
+    ka = _f64(np.concatenate([it["k"] for it in items]))
+    va = _f64(np.concatenate([it["v"] for it in items]))
+    out = np.zeros((int(nq.sum()), D))
+    lse = np.zeros(int(nq.sum()))
+    sec = C.c_double()
+    rc = ref().dcpr_run_items(n, _p(nq), _p(nk), _p(row_off), _p(rows), D, _p(qa), _p(ka), _p(va),
+                              _p(row_off), _p(k_off), _p(row_off), _p(out), _p(lse), threads, C.byref(sec))
+    if rc:
+        raise RuntimeError(ref().dcpr_last_error().decode())
+    outs = [out[o:o + a] for o, a in zip(row_off, nq)]
+    lses = [lse[o:o + a] for o, a in zip(row_off, nq)]
+    return outs, lses, sec.value

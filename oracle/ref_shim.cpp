@@ -10,6 +10,7 @@
 //   dcpr_time_items    exec_attention over a deterministic sample of a plan's
 //                      AttentionItems on N host threads (CPU baseline)
 #include <atomic>
+#include <limits>
 #include <chrono>
 #include <cstring>
 #include <string>
@@ -326,6 +327,46 @@ int dcpr_time_items(int n, const int32_t* nq, const int32_t* nk, const int64_t* 
       });
     for (auto& th : pool) th.join();
     *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
+}
+
+// CPU baseline with outputs: the same as dcpr_time_items, but on the caller's inputs (item i
+// reads nq[i] x D rows of q at q + D * in_off_q[i], nk[i] x D rows of k and v at
+// k / v + D * in_off_k[i]) and returning item i's (out, LSE = m + ln l; -inf where l = 0) at
+// out + D * out_off[i] / lse + out_off[i], so the timed sample can be checked against the GPU.
+int dcpr_run_items(int n, const int32_t* nq, const int32_t* nk, const int64_t* row_off, const int32_t* rows,
+                   int D, const double* q, const double* k, const double* v, const int64_t* in_off_q,
+                   const int64_t* in_off_k, const int64_t* out_off, double* out, double* lse, int threads,
+                   double* seconds) {
+  try {
+    std::vector<dcp::Matrix> qs, ks, vs;
+    std::vector<std::vector<dcp::TokenRanges>> rr;
+    for (int i = 0; i < n; ++i) {
+      qs.push_back(to_matrix(q + D * in_off_q[i], nq[i], D));
+      ks.push_back(to_matrix(k + D * in_off_k[i], nk[i], D));
+      vs.push_back(to_matrix(v + D * in_off_k[i], nk[i], D));
+      rr.push_back(to_rows(rows + 4 * row_off[i], nq[i]));
+    }
+    std::vector<dcp::PartialBlock> res(static_cast<size_t>(n));
+    std::atomic<int> next{0};
+    const auto t0 = std::chrono::steady_clock::now();
+    std::vector<std::thread> pool;
+    for (int t = 0; t < threads; ++t)
+      pool.emplace_back([&] {
+        int i;
+        while ((i = next.fetch_add(1)) < n) res[static_cast<size_t>(i)] = dcp::exec_attention(qs[i], ks[i], vs[i], rr[i]);
+      });
+    for (auto& th : pool) th.join();
+    *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    for (int i = 0; i < n; ++i) {
+      const auto& p = res[static_cast<size_t>(i)];
+      std::memcpy(out + D * out_off[i], p.out.a.data(), sizeof(double) * static_cast<size_t>(nq[i]) * D);
+      for (int r = 0; r < nq[i]; ++r)
+        lse[out_off[i] + r] = p.l[r] > 0 ? p.m[r] + std::log(p.l[r]) : -std::numeric_limits<double>::infinity();
+    }
     return 0;
   } catch (const std::exception& e) {
     return fail(e);

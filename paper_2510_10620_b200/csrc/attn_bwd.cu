@@ -506,8 +506,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         named_bar_sync(2, 128);
         if (wq == 0) {
           if (elect_one()) {
-            if (!(p.debug_flags & 1))
-              for (int k = 0; k < 4; ++k) tma_reduce_add_2d(&tm_dq, sEpi + k * 8192, 32 * k, q_row0);
+            for (int k = 0; k < 4; ++k) tma_reduce_add_2d(&tm_dq, sEpi + k * 8192, 32 * k, q_row0);
             bulk_commit();
           }
           __syncwarp();

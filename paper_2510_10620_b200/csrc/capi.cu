@@ -1,6 +1,7 @@
 // capi.cu — extern "C" boundary (include/dcpx.h). No exception crosses it: every
 // dcpx::Failure maps onto its dcpx_status, mirroring the reference's exception types
 // (types.hpp:17-45); the message is kept per context (dcpx_last_error).
+#include <algorithm>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -103,6 +104,38 @@ dcpx_status dcpx_synchronize(dcpx_ctx* ctx) {
   return guarded(ctx, [&](dcpx::Executor& ex) { ex.synchronize(); });
 }
 
+dcpx_status dcpx_set_streams(dcpx_ctx* ctx, int n, void* const* streams) {
+  return guarded(ctx, [&](dcpx::Executor& ex) {
+    if (n < 0 || (n > 0 && !streams)) throw dcpx::Failure(DCPX_ERROR, "dcpx_set_streams: bad stream array");
+    std::vector<cudaStream_t> s(static_cast<size_t>(n));
+    for (int i = 0; i < n; ++i) s[i] = static_cast<cudaStream_t>(streams[i]);
+    ex.set_streams(n, s.data());
+  });
+}
+
+dcpx_status dcpx_check_plans(int nplans, const dcpx_plan_view* plans, const dcpx_graph_view* graph,
+                             const dcpx_mask_view* masks, char* err, int64_t cap) {
+  std::string msg;
+  dcpx_status st = DCPX_OK;
+  try {
+    if (!plans || !graph || !masks) throw dcpx::Failure(DCPX_ERROR, "dcpx_check_plans: null view");
+    dcpx::Executor ex(nplans, nullptr);  // host-only: no GPU is touched
+    ex.prepare(nplans, plans, graph, masks);
+  } catch (const dcpx::Failure& e) {
+    st = e.code;
+    msg = e.what();
+  } catch (const std::exception& e) {
+    st = DCPX_ERROR;
+    msg = e.what();
+  }
+  if (err && cap > 0) {
+    const size_t n = std::min<size_t>(msg.size(), static_cast<size_t>(cap - 1));
+    std::memcpy(err, msg.data(), n);
+    err[n] = '\0';
+  }
+  return st;
+}
+
 dcpx_status dcpx_debug_arena(dcpx_ctx* ctx, int dev, int kind, void** ptr, int64_t* slot_rows) {
   return guarded(ctx, [&](dcpx::Executor& ex) { ex.debug_arena(dev, kind, ptr, slot_rows); });
 }
@@ -122,7 +155,6 @@ dcpx_status dcpx_set_option(dcpx_ctx* ctx, const char* key, int64_t value) {
     else if (k == "bwd_merge_heads") ex.opt.bwd_merge_heads = static_cast<int>(value);
     else if (k == "sm_reserve") ex.opt.sm_reserve = static_cast<int>(value);
     else if (k == "kernel_timing") ex.opt.kernel_timing = value != 0;
-    else if (k == "bwd_debug") ex.opt.bwd_debug = static_cast<int>(value);
     else throw dcpx::Failure(DCPX_ERROR, "unknown option " + k);
   });
 }

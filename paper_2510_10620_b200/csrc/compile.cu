@@ -87,6 +87,7 @@ void Executor::compile_device(int d) {
   DevState& D = dev_[d];
   const int64_t SR = D.slot_rows;
   D.prog.assign(P.ins.size(), Op{});
+  D.bwd_units = D.bwd_windowed = 0;
 
   // ---- 1. fusion decisions for attention + reductions
   std::vector<bool> fused_red(P.ins.size(), false);
@@ -468,6 +469,8 @@ void Executor::compile_device(int d) {
         op.bsteps = upload(d, bsteps);
         op.bitems = op.items;
         op.bnum_units = static_cast<int>(bsorted.size());
+        D.bwd_units += op.bnum_units;
+        D.bwd_windowed += windowed ? 1 : 0;
         op.bgrid = std::min(op.bnum_units, num_sms(D.ordinal));
         if (I.division >= 0 && I.division < static_cast<int>(comp_flops_.size())) comp_flops_[I.division][d] += op.flops;
         break;
@@ -635,6 +638,8 @@ void Executor::build_bwd_jobs() {
   const int64_t TT = g_.total_tokens(), H = g_.H, G = g_.G;
   bwd_send_.assign(static_cast<size_t>(R_), 0);
   bwd_recv_.assign(static_cast<size_t>(R_), 0);
+  wire_bwd_send_.assign(static_cast<size_t>(R_), 0);
+  wire_bwd_recv_.assign(static_cast<size_t>(R_), 0);
   std::map<int, std::pair<int, int>> owner;  // resident Q / KV block -> (device, slot)
   for (int d = 0; d < R_; ++d) {
     for (const auto& r : plans_[d].res_q) owner[r.block] = {d, r.slot};
@@ -672,54 +677,67 @@ void Executor::build_bwd_jobs() {
           jobs.push_back({reinterpret_cast<const char*>(A.delta + sb.slot * SR), reinterpret_cast<char*>(D.delta + rb.slot * SR), 4 * rows, 4 * rows, 1, 4 * rows});
           bwd_send_[src_dev] += 2 * db.size_bytes; bwd_recv_[d] += 2 * db.size_bytes;  // Q + dO out
           bwd_send_[d] += db.size_bytes; bwd_recv_[src_dev] += db.size_bytes;          // dQ back
+          const uint64_t out = 2 * db.size_bytes + 8 * static_cast<uint64_t>(rows);     // + fp32 LSE, Delta
+          wire_bwd_send_[src_dev] += out; wire_bwd_recv_[d] += out;
+          wire_bwd_send_[d] += 2 * db.size_bytes; wire_bwd_recv_[src_dev] += 2 * db.size_bytes;  // fp32 dQ
         } else if (db.kind == DCPX_KIND_KV) {
           for (int h = 0; h < 2; ++h)
             jobs.push_back({reinterpret_cast<const char*>(A.kv + (2 * sb.slot + h) * SR * 128),
                             reinterpret_cast<char*>(D.kv + (2 * rb.slot + h) * SR * 128), 256, 256, rows, 256});
           bwd_send_[src_dev] += db.size_bytes; bwd_recv_[d] += db.size_bytes;  // K, V out
           bwd_send_[d] += db.size_bytes; bwd_recv_[src_dev] += db.size_bytes;  // dK, dV back
+          wire_bwd_send_[src_dev] += db.size_bytes; wire_bwd_recv_[d] += db.size_bytes;
+          wire_bwd_send_[d] += 2 * db.size_bytes; wire_bwd_recv_[src_dev] += 2 * db.size_bytes;  // fp32 dK, dV
         }
       }
       op.bjobs = make_jobs(d, jobs);
       op.bxfer = jobs;
     }
-    // 2. gradient returns of fetched blocks, right after the attention of their last use
-    std::map<int, int> cur_q, cur_kv;                    // slot -> fetched block
-    std::map<int, std::pair<size_t, int>> last_q, last_kv;  // block -> (attention instr, slot)
+    // 2. gradient returns of fetched blocks, right after the attention of their last use.
+    //    One fetch episode per receive of a block into a slot (a plan may fetch the same
+    //    block twice, into different slots or at different divisions): each episode's
+    //    accumulator is returned (and zeroed) after its own last use.
+    struct Episode { int block, slot, kind; size_t last; bool used; };
+    std::vector<Episode> eps;
+    std::map<int, int> cur_q, cur_kv;  // slot -> episode
     for (size_t i = 0; i < P.ins.size(); ++i) {
       const Instr& I = P.ins[i];
       if (I.op == DCPX_OP_COMM_LAUNCH && !I.send && I.division < T) {
         for (int b = 0; b < I.count; ++b) {
           const auto tb = P.blocks[I.offset + b];
           const int k = g_.data_blocks[tb.block].kind;
-          if (k == DCPX_KIND_Q) cur_q[tb.slot] = tb.block;
-          else if (k == DCPX_KIND_KV) cur_kv[tb.slot] = tb.block;
+          if (k != DCPX_KIND_Q && k != DCPX_KIND_KV) continue;
+          (k == DCPX_KIND_Q ? cur_q : cur_kv)[tb.slot] = static_cast<int>(eps.size());
+          eps.push_back({tb.block, tb.slot, k, 0, false});
         }
       } else if (I.op == DCPX_OP_ATTENTION) {
         for (int k = 0; k < I.count; ++k) {
           const auto& it = P.items[I.offset + k];
-          auto q = cur_q.find(it.q_slot);
-          if (q != cur_q.end()) last_q[q->second] = {i, it.q_slot};
-          auto kv = cur_kv.find(it.kv_slot);
-          if (kv != cur_kv.end()) last_kv[kv->second] = {i, it.kv_slot};
+          for (auto* cur : {&cur_q, &cur_kv}) {
+            auto e = cur->find(cur == &cur_q ? it.q_slot : it.kv_slot);
+            if (e != cur->end()) {
+              eps[e->second].last = i;
+              eps[e->second].used = true;
+            }
+          }
         }
       }
     }
     std::map<size_t, std::vector<RowCopyJob>> ret;
-    for (const auto& [block, use] : last_q) {
-      const auto [o, so] = owner.at(block);
-      const auto& db = g_.data_blocks[block];
-      ret[use.first].push_back({reinterpret_cast<const char*>(D.dq_acc + use.second * SR * 128),
-                                reinterpret_cast<char*>(dev_[o].dq_acc + so * SR * 128), 512, 512,
-                                static_cast<int32_t>(db.tok_end - db.tok_begin), 512});
-    }
-    for (const auto& [block, use] : last_kv) {
-      const auto [o, so] = owner.at(block);
-      const auto& db = g_.data_blocks[block];
-      for (int h = 0; h < 2; ++h)
-        ret[use.first].push_back({reinterpret_cast<const char*>(D.dkv_acc + (2 * use.second + h) * SR * 128),
+    for (const auto& ep : eps) {
+      if (!ep.used) continue;  // never read: its accumulator stays zero
+      const auto [o, so] = owner.at(ep.block);
+      const auto& db = g_.data_blocks[ep.block];
+      const int rows = static_cast<int>(db.tok_end - db.tok_begin);
+      if (ep.kind == DCPX_KIND_Q) {
+        ret[ep.last].push_back({reinterpret_cast<const char*>(D.dq_acc + ep.slot * SR * 128),
+                                reinterpret_cast<char*>(dev_[o].dq_acc + so * SR * 128), 512, 512, rows, 512});
+      } else {
+        for (int h = 0; h < 2; ++h)
+          ret[ep.last].push_back({reinterpret_cast<const char*>(D.dkv_acc + (2 * ep.slot + h) * SR * 128),
                                   reinterpret_cast<char*>(dev_[o].dkv_acc + (2 * so + h) * SR * 128), 512, 512,
-                                  static_cast<int32_t>(db.tok_end - db.tok_begin), 512});
+                                  rows, 512});
+      }
     }
     for (auto& [i, jobs] : ret) D.prog[i].ret = make_jobs(d, jobs);
     // 3. io: dO scatter to the resident Q slots, Delta/LSE preprocess, gradient gathers

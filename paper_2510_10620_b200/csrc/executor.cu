@@ -36,6 +36,11 @@ Executor::Executor(int ndev, const int* ordinals, int transport, int rank)
   if (rank_ >= 0 && (rank_ >= ndev || transport != DCPX_TRANSPORT_LOCAL))
     throw Failure(DCPX_ERROR, "per-rank mode: rank outside the plan, or a transport other than peer memory");
   if (ndev < 1 || ndev > 64) throw Failure(DCPX_ERROR, "dcpx_create: 1..64 devices supported");
+  if (!ordinals) {  // host-only: plan verification and the lockstep replay, no GPU
+    host_only_ = true;
+    dev_.resize(static_cast<size_t>(ndev));
+    return;
+  }
   ordinals_.assign(ordinals, ordinals + ndev);
   int count = 0;
   CUDA_OK(cudaGetDeviceCount(&count));
@@ -70,6 +75,8 @@ Executor::Executor(int ndev, const int* ordinals, int transport, int rank)
     CUDA_OK(cudaStreamCreateWithPriority(&dev_[d].ms, cudaStreamNonBlocking, hi));  // transfers first
     CUDA_OK(cudaEventCreate(&dev_[d].t0));
     CUDA_OK(cudaEventCreate(&dev_[d].t1));
+    CUDA_OK(cudaEventCreateWithFlags(&dev_[d].ev_join, cudaEventDisableTiming));
+    CUDA_OK(cudaEventCreateWithFlags(&dev_[d].ev_done, cudaEventDisableTiming));
   }
   if (R_ > 0) {
     DeviceGuard g(ordinals_[0]);
@@ -124,10 +131,38 @@ void Executor::await_peer_pulls() {
     return;
   }
   if (pulls_done_.empty() || R_ < 2) return;
+  // plan devices sharing one GPU run on separate non-blocking streams, so they need the
+  // wait as much as devices on different GPUs do
   for (int d = 0; d < R_; ++d) {
     DeviceGuard g(dev_[d].ordinal);
     for (int e = 0; e < R_; ++e)
-      if (e != d && dev_[e].ordinal != dev_[d].ordinal) CUDA_OK(cudaStreamWaitEvent(dev_[d].cs, pulls_done_[e], 0));
+      if (e != d) CUDA_OK(cudaStreamWaitEvent(dev_[d].cs, pulls_done_[e], 0));
+  }
+}
+
+void Executor::set_streams(int n, const cudaStream_t* s) {
+  if (host_only_) throw Failure(DCPX_ERROR, "host-only context");
+  if (n != R_) throw Failure(DCPX_ERROR, "dcpx_set_streams: one stream per plan device");
+  for (int d = 0; d < R_; ++d) dev_[d].caller = s[d] ? s[d] : cudaStreamLegacy;
+}
+
+void Executor::join_caller() {
+  for (int d = 0; d < R_; ++d) {
+    if (!local(d)) continue;
+    DevState& D = dev_[d];
+    DeviceGuard g(D.ordinal);
+    CUDA_OK(cudaEventRecord(D.ev_join, D.caller));
+    CUDA_OK(cudaStreamWaitEvent(D.cs, D.ev_join, 0));
+  }
+}
+
+void Executor::release_caller() {
+  for (int d = 0; d < R_; ++d) {
+    if (!local(d)) continue;
+    DevState& D = dev_[d];
+    DeviceGuard g(D.ordinal);
+    CUDA_OK(cudaEventRecord(D.ev_done, D.cs));
+    CUDA_OK(cudaStreamWaitEvent(D.caller, D.ev_done, 0));
   }
 }
 
@@ -157,6 +192,7 @@ cudaEvent_t Executor::staging_event(int d) {
 }
 
 Executor::~Executor() {
+  if (host_only_) return;
   for (auto& d : dev_) {
     DeviceGuard g(d.ordinal);
     if (d.cs) cudaStreamSynchronize(d.cs);
@@ -181,6 +217,9 @@ Executor::~Executor() {
     DeviceGuard g(d.ordinal);
     for (auto e : d.events) cudaEventDestroy(e);
     for (auto& e : d.kev) { cudaEventDestroy(e.first); cudaEventDestroy(e.second); }
+    for (auto& e : d.tev) { cudaEventDestroy(e.first); cudaEventDestroy(e.second); }
+    if (d.ev_join) cudaEventDestroy(d.ev_join);
+    if (d.ev_done) cudaEventDestroy(d.ev_done);
     if (d.t0) cudaEventDestroy(d.t0);
     if (d.t1) cudaEventDestroy(d.t1);
     if (d.cs) cudaStreamDestroy(d.cs);
@@ -255,7 +294,7 @@ void Executor::trace_begin() {
 TraceScope::TraceScope(Executor* ex, int d, int instr, cudaStream_t s, int pass, const Op& op)
     : ex_(ex), d_(d) {
   if (!ex->opt.trace || op.kind == OpKind::kNop) return;
-  auto ev = ex->kernel_events(d);
+  auto ev = ex->trace_events(d);
   CUDA_OK(cudaEventRecord(ev.first, s));
   ex->trace_pending_.push_back({d, instr, static_cast<int>(op.kind), op.division, pass, ev.first, ev.second});
   s_ = s;
@@ -268,7 +307,7 @@ TraceScope::~TraceScope() {
 
 void TraceScope::split(int kind) {
   if (!active_) return;
-  auto ev = ex_->kernel_events(d_);
+  auto ev = ex_->trace_events(d_);
   CUDA_OK(cudaEventRecord(ev.first, s_));
   Executor::TracePending prev = ex_->trace_pending_.back();
   ex_->trace_pending_.back().end = ev.first;
@@ -307,6 +346,18 @@ int Executor::trace_rows(double* out, int max_rows) const {
   return static_cast<int>(trace_.size());
 }
 
+std::pair<cudaEvent_t, cudaEvent_t> Executor::trace_events(int d) {
+  auto& D = dev_[d];
+  if (D.next_tev == D.tev.size()) {
+    DeviceGuard g(D.ordinal);
+    cudaEvent_t a, b;
+    CUDA_OK(cudaEventCreate(&a));
+    CUDA_OK(cudaEventCreate(&b));
+    D.tev.push_back({a, b});
+  }
+  return D.tev[D.next_tev++];
+}
+
 std::pair<cudaEvent_t, cudaEvent_t> Executor::kernel_events(int d) {
   auto& D = dev_[d];
   if (D.next_kev == D.kev.size()) {
@@ -323,7 +374,7 @@ std::pair<cudaEvent_t, cudaEvent_t> Executor::kernel_events(int d) {
 void Executor::prepare(int nplans, const dcpx_plan_view* plans, const dcpx_graph_view* gv,
                        const dcpx_mask_view* mv) {
   if (nplans != R_) throw Failure(DCPX_ERROR, "run: plan count does not match topology");  // simexec.hpp:211
-  synchronize();  // asynchronous host I/O of a previous plan may still be in flight
+  if (!host_only_) synchronize();  // asynchronous host I/O of a previous plan may still be in flight
   if (rank_ >= 0) {  // per-rank mode: the previous plan's peer mappings and flags
     DeviceGuard g(dev_[rank_].ordinal);
     for (void* p : ipc_mapped_) cudaIpcCloseMemHandle(p);
@@ -332,9 +383,8 @@ void Executor::prepare(int nplans, const dcpx_plan_view* plans, const dcpx_graph
     flags_ = nullptr;
     connected_ = false;
   }
-  free_all();
-  out_stage_ = nullptr;
-  for (Staging* st : {&in_st_, &bwd_st_})
+  if (!host_only_) free_all();
+  for (Staging* st : {&in_st_, &bwd_st_, &fwd_st_})
     for (int k = 0; k < 2; ++k) {  // (events stay alive in staging_events_ and are reused)
       st->buf[k] = nullptr;
     }
@@ -347,8 +397,9 @@ void Executor::prepare(int nplans, const dcpx_plan_view* plans, const dcpx_graph
   // ---- graph copy
   g_ = GraphCopy{};
   g_.H = gv->heads; g_.G = gv->kv_groups; g_.D = gv->head_dim; g_.bpe = gv->bytes_per_element;
-  if (g_.D != kHeadDim) throw Failure(DCPX_UNSUPPORTED, "sm_100a kernels support head_dim 128 only");
-  if (g_.bpe != 2) throw Failure(DCPX_UNSUPPORTED, "bf16 payloads (bytes_per_element 2) only");
+  // (a host-only context executes nothing, so any head_dim / element size verifies)
+  if (!host_only_ && g_.D != kHeadDim) throw Failure(DCPX_UNSUPPORTED, "sm_100a kernels support head_dim 128 only");
+  if (!host_only_ && g_.bpe != 2) throw Failure(DCPX_UNSUPPORTED, "bf16 payloads (bytes_per_element 2) only");
   if (g_.H < 1 || g_.G < 1 || g_.H % g_.G) throw Failure(DCPX_ERROR, "batch: heads must be divisible by kv_groups");
   g_.seq_lengths.assign(gv->seq_lengths, gv->seq_lengths + gv->num_seqs);
   g_.block_sizes.assign(gv->block_sizes, gv->block_sizes + gv->num_seqs);
@@ -510,6 +561,10 @@ void Executor::prepare(int nplans, const dcpx_plan_view* plans, const dcpx_graph
 
   // ---- lockstep replay: deadlock / tag errors + the global issue order
   simulate_order();
+  if (host_only_) {
+    prepared_ = true;
+    return;
+  }
 
   // ---- per-device compile
   for (int d = 0; d < R_; ++d) {
@@ -677,6 +732,8 @@ void Executor::simulate_order() {
   const int T = R_ ? plans_[0].divisions : 0;
   comm_bytes_.assign(static_cast<size_t>(T) + 1, {});
   comp_flops_.assign(static_cast<size_t>(T) + 1, std::vector<uint64_t>(static_cast<size_t>(R_), 0));
+  wire_fwd_send_.assign(static_cast<size_t>(R_), 0);
+  wire_fwd_recv_.assign(static_cast<size_t>(R_), 0);
   std::vector<size_t> pc(static_cast<size_t>(R_), 0);
   std::map<std::string, std::pair<int, int>> inbox;  // tag -> (src, dst)
   std::vector<std::set<std::string>> posted(static_cast<size_t>(R_));
@@ -700,9 +757,16 @@ void Executor::simulate_order() {
           if (I.send) {
             if (!inbox.insert({I.tag, {d, I.peer}}).second)
               throw Failure(DCPX_TAG_MISMATCH, "duplicate message tag " + I.tag);
-            uint64_t bytes = 0;
-            for (int b = 0; b < I.count; ++b) bytes += g_.data_blocks[P.blocks[I.offset + b].block].size_bytes;
+            uint64_t bytes = 0, wire = 0;
+            for (int b = 0; b < I.count; ++b) {
+              const auto& db = g_.data_blocks[P.blocks[I.offset + b].block];
+              bytes += db.size_bytes;
+              // an O block travels with its fp32 LSE rows (the reference moves (out, m, l))
+              wire += db.size_bytes + (db.kind == DCPX_KIND_O ? 4 * static_cast<uint64_t>(db.tok_end - db.tok_begin) : 0);
+            }
             if (I.division >= 0 && I.division <= T) comm_bytes_[I.division][{d, I.peer}] += bytes;
+            wire_fwd_send_[d] += wire;
+            wire_fwd_recv_[I.peer] += wire;
           } else {
             posted[d].insert(I.tag);
           }

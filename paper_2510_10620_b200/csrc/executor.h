@@ -115,14 +115,21 @@ struct DevState {
   int launches = 0;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> kev;  // per attention launch (kernel_timing)
   size_t next_kev = 0;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> tev;  // per traced op (trace), a separate pool
+  size_t next_tev = 0;
+  // stream contract with the caller: every call starts after the work already enqueued on
+  // `caller` (its inputs) and `caller` waits for the call's device work (its outputs)
+  cudaStream_t caller = cudaStreamLegacy;
+  cudaEvent_t ev_join = nullptr, ev_done = nullptr;
+  // backward units of the last prepare (diagnostics in the report)
+  int32_t bwd_units = 0, bwd_windowed = 0;
 };
 
 struct Options {
   bool fuse_reductions = true;
   bool remap_copies = true;
   bool check_rows = false;
-  bool timing = true;
-  int bwd_debug = 0;
+  bool timing = false;  // per-call device_ms in the report (blocks the host at the end of each call)
   bool kernel_timing = false;
   bool trace = false;
   bool sm_transfers = true;   // LOCAL transfers by copy kernel (false: DMA copy engines)
@@ -165,6 +172,9 @@ class Executor {
   // per-rank mode (one process per GPU): all ordinals are this process's GPU, only plan
   // device `rank` executes, peers' arenas are mapped over CUDA IPC (export / connect).
   Executor(int ndev, const int* ordinals, int transport = DCPX_TRANSPORT_LOCAL, int rank = -1);
+  // host-only instance (ordinals == nullptr): prepare() ingests, verifies and replays the plans
+  // (verify_plans + the lockstep deadlock / tag checks) without touching a GPU
+  bool host_only() const { return host_only_; }
   // per-rank mode: IPC handles of this rank's arenas and flags; map every peer's
   int64_t export_handles(void* buf, int64_t cap) const;
   void connect(const void* blobs, int64_t blob_size, int world);
@@ -182,6 +192,8 @@ class Executor {
   void backward(const void* const* d_o, void* const* dq, void* const* dk, void* const* dv, dcpx_report* rep,
                 bool host);
   void synchronize();
+  // the caller's stream on each plan device (nullptr entry: the legacy default stream)
+  void set_streams(int n, const cudaStream_t* s);
   void debug_arena(int dev, int kind, void** ptr, int64_t* rows);
   int trace_rows(double* out, int max_rows) const;
   std::string watchdog_info() const;  // barrier waits that timed out (kernel watchdog)  // rows of 7: dev, instr, kind, division, pass, start_ms, end_ms
@@ -208,9 +220,13 @@ class Executor {
   void simulate_order();
   cudaEvent_t event(int d);
   std::pair<cudaEvent_t, cudaEvent_t> kernel_events(int d);
+  std::pair<cudaEvent_t, cudaEvent_t> trace_events(int d);
+  void join_caller();     // cs of every local device waits for the caller's stream
+  void release_caller();  // the caller's stream waits for cs of every local device
   void free_all();
 
   int R_ = 0;
+  bool host_only_ = false;
   std::vector<int> ordinals_;
   std::vector<PlanCopy> plans_;
   GraphCopy g_;
@@ -255,8 +271,7 @@ class Executor {
     cudaEvent_t up[2] = {nullptr, nullptr};  // upload into slot k finished (h2d_)
     int next = 0;
   };
-  Staging in_st_, bwd_st_;
-  char* out_stage_ = nullptr;  // host-output staging on device 0 (forward_host, synchronous)
+  Staging in_st_, bwd_st_, fwd_st_;  // fwd_st_: forward_host outputs (O + LSE), downloaded on d2h_
   cudaStream_t h2d_ = nullptr, d2h_ = nullptr;  // on device 0
   cudaEvent_t staging_event(int d);              // persistent (not from the per-call pool)
   // pulls_done_[d]: recorded on device d's comm stream at the end of each pass (its last
@@ -269,6 +284,8 @@ class Executor {
   std::vector<int> staging_event_dev_;
   bool fwd_done_ = false;
   std::vector<uint64_t> bwd_send_, bwd_recv_;  // planned backward bytes per device
+  // bytes the transfers actually move (fp32 sidecars and fp32 gradient returns included)
+  std::vector<uint64_t> wire_fwd_send_, wire_fwd_recv_, wire_bwd_send_, wire_bwd_recv_;
   bool prepared_ = false;
   // report
   std::vector<std::map<std::pair<int, int>, uint64_t>> comm_bytes_;

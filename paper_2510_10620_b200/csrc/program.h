@@ -97,8 +97,7 @@ struct BwdParams {
   int32_t slot_rows;
   float scale_log2;
   float scale;
-  int32_t debug_flags;  // bit0: skip the dQ reduce-add (timing experiments only)
-  int32_t _pad;
+  int32_t _pad0, _pad1;
 };
 
 struct FwdParams {

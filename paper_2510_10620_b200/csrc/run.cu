@@ -44,6 +44,7 @@ void Executor::copy_ranges(void* dst, const void* src, const std::vector<std::pa
 }
 
 void Executor::load_inputs(const void* const* q, const void* const* k, const void* const* v, bool host) {
+  if (host_only_) throw Failure(DCPX_ERROR, "host-only context: nothing executes");
   if (!prepared_) throw Failure(DCPX_ERROR, "dcpx_load_inputs before dcpx_prepare");
   if (rank_ >= 0 && !connected_) throw Failure(DCPX_ERROR, "dcpx_load_inputs: per-rank context not connected (dcpx_rank_connect)");
   const int64_t TT = g_.total_tokens();
@@ -77,6 +78,7 @@ void Executor::load_inputs(const void* const* q, const void* const* k, const voi
     std::fill(sk.begin(), sk.end(), buf + bq);
     std::fill(sv.begin(), sv.end(), buf + bq + bk);
   }
+  join_caller();       // device inputs are produced on the caller's stream
   await_peer_pulls();  // resident slots may still be read by a peer's previous-call pull
   for (int d = 0; d < R_; ++d) {
     if (!local(d)) continue;
@@ -97,21 +99,24 @@ void Executor::load_inputs(const void* const* q, const void* const* k, const voi
       CUDA_OK(cudaEventRecord(fr[d], dev_[d].cs));
     }
   }
+  release_caller();  // the caller may overwrite its input buffers after this point
 }
 
 void Executor::forward(void* const* o_out, float* const* lse_out, dcpx_report* rep, bool host) {
+  if (host_only_) throw Failure(DCPX_ERROR, "host-only context: nothing executes");
   if (!prepared_) throw Failure(DCPX_ERROR, "dcpx_forward before dcpx_prepare");
   if (rank_ >= 0 && !connected_) throw Failure(DCPX_ERROR, "dcpx_forward: per-rank context not connected (dcpx_rank_connect)");
-  if (rank_ >= 0 && !connected_) throw Failure(DCPX_ERROR, "per-rank context: connect before forward");
   const int64_t TT = g_.total_tokens();
+  join_caller();  // the output buffers may still be in use on the caller's stream
   for (int d = 0; d < R_; ++d) {
     DevState& D = dev_[d];
     D.next_event = 0;
     D.next_kev = 0;
+    D.next_tev = 0;
     D.launches = 0;
     if (!local(d)) continue;
     DeviceGuard gd(D.ordinal);
-    if (opt.timing) CUDA_OK(cudaEventRecord(D.t0, D.cs));
+    if (opt.timing || opt.trace) CUDA_OK(cudaEventRecord(D.t0, D.cs));
   }
   await_peer_pulls();
   ++epoch_;
@@ -201,10 +206,22 @@ void Executor::forward(void* const* o_out, float* const* lse_out, dcpx_report* r
     l_dev[d] = reinterpret_cast<char*>(lse_out ? lse_out[d] : nullptr);
   }
   const bool want_o = o_dev[0] != nullptr, want_l = l_dev[0] != nullptr;
+  int slot = -1;
   if (host && (want_o || want_l)) {
-    if (!out_stage_) out_stage_ = static_cast<char*>(alloc(0, TT * g_.H * 256 + TT * g_.H * 4));
-    std::fill(o_dev.begin(), o_dev.end(), want_o ? out_stage_ : nullptr);
-    std::fill(l_dev.begin(), l_dev.end(), want_l ? out_stage_ + TT * g_.H * 256 : nullptr);
+    // asynchronous like the other host calls: gather into device-0 staging slot k (once
+    // the slot's previous download is done), download on d2h_; host buffers are valid after
+    // dcpx_synchronize, so the download overlaps the next call's work
+    slot = fwd_st_.next;
+    fwd_st_.next ^= 1;
+    char*& buf = fwd_st_.buf[slot];
+    if (!buf) buf = static_cast<char*>(alloc(0, TT * g_.H * 256 + TT * g_.H * 4));
+    for (int d = 0; d < R_; ++d) {
+      if (!local(d)) continue;
+      DeviceGuard gd(dev_[d].ordinal);
+      for (cudaEvent_t e : fwd_st_.free[slot]) CUDA_OK(cudaStreamWaitEvent(dev_[d].cs, e, 0));
+    }
+    std::fill(o_dev.begin(), o_dev.end(), want_o ? buf : nullptr);
+    std::fill(l_dev.begin(), l_dev.end(), want_l ? buf + TT * g_.H * 256 : nullptr);
   }
   for (int d = 0; d < R_; ++d) {
     if (!local(d)) continue;
@@ -215,26 +232,28 @@ void Executor::forward(void* const* o_out, float* const* lse_out, dcpx_report* r
     if (opt.timing) CUDA_OK(cudaEventRecord(D.t1, D.cs));
     CUDA_OK(cudaGetLastError());
   }
-  if (host && (want_o || want_l)) {
+  if (slot >= 0) {
     DevState& D0 = dev_[0];
-    DeviceGuard gd(D0.ordinal);
-    for (int d = 1; d < R_; ++d) {
+    for (int d = 0; d < R_; ++d) {  // every device's gathers into the slot are done
       if (!local(d)) continue;
       cudaEvent_t e = event(d);
       DeviceGuard g2(dev_[d].ordinal);
       CUDA_OK(cudaEventRecord(e, dev_[d].cs));
-      DeviceGuard g3(D0.ordinal);
-      CUDA_OK(cudaStreamWaitEvent(D0.cs, e, 0));
+      CUDA_OK(cudaStreamWaitEvent(d2h_, e, 0));
     }
+    DeviceGuard gd(D0.ordinal);
     const auto ro = host_ranges(2);
-    if (want_o) copy_ranges(o_out[0], o_dev[0], ro, g_.H * 256, cudaMemcpyDeviceToHost, D0.cs);
+    if (want_o) copy_ranges(o_out[0], o_dev[0], ro, g_.H * 256, cudaMemcpyDeviceToHost, d2h_);
     if (want_l)  // LSE is head-major [H][T]: one strided copy per token range
       for (const auto& [b, e] : ro)
         if (e > b)
           CUDA_OK(cudaMemcpy2DAsync(static_cast<char*>(static_cast<void*>(lse_out[0])) + b * 4, TT * 4, l_dev[0] + b * 4,
-                                    TT * 4, (e - b) * 4, g_.H, cudaMemcpyDeviceToHost, D0.cs));
-    CUDA_OK(cudaStreamSynchronize(D0.cs));
+                                    TT * 4, (e - b) * 4, g_.H, cudaMemcpyDeviceToHost, d2h_));
+    auto& fr = fwd_st_.free[slot];
+    if (fr.empty()) fr.push_back(staging_event(0));
+    CUDA_OK(cudaEventRecord(fr[0], d2h_));
   }
+  release_caller();  // o_out / lse_out are ready in the caller's stream order
   fill_report(rep, false);
   fwd_done_ = true;
 }
@@ -279,8 +298,16 @@ void Executor::fill_report(dcpx_report* rep, bool bwd) {
       rep->total_bytes += bwd_send_[d];
     }
   }
-  rep->wire_bytes = rep->total_bytes;
-  for (int d = 0; d < R_; ++d) rep->kernel_launches += dev_[d].launches;
+  for (int d = 0; d < R_; ++d) {
+    rep->wire_per_device_send[d] = bwd ? wire_bwd_send_[d] : wire_fwd_send_[d];
+    rep->wire_per_device_recv[d] = bwd ? wire_bwd_recv_[d] : wire_fwd_recv_[d];
+    rep->wire_bytes += rep->wire_per_device_send[d];
+    rep->kernel_launches += dev_[d].launches;
+    if (!local(d)) continue;
+    for (const Op& op : dev_[d].prog)
+      if (op.kind == OpKind::kFwdAttn) rep->units += bwd ? op.bnum_units : op.num_units;
+    if (bwd) rep->windowed += dev_[d].bwd_windowed;
+  }
   if (opt.kernel_timing) {
     double mx = 0;
     for (int d = 0; d < R_; ++d) {
@@ -317,6 +344,7 @@ void Executor::fill_report(dcpx_report* rep, bool bwd) {
 
 void Executor::backward(const void* const* d_o, void* const* dq, void* const* dk, void* const* dv,
                         dcpx_report* rep, bool host) {
+  if (host_only_) throw Failure(DCPX_ERROR, "host-only context: nothing executes");
   if (!prepared_) throw Failure(DCPX_ERROR, "dcpx_backward before dcpx_prepare");
   if (rank_ >= 0 && !connected_) throw Failure(DCPX_ERROR, "dcpx_backward: per-rank context not connected (dcpx_rank_connect)");
   if (!fwd_done_) throw Failure(DCPX_ERROR, "dcpx_backward needs a preceding dcpx_forward");
@@ -331,14 +359,16 @@ void Executor::backward(const void* const* d_o, void* const* dq, void* const* dk
     ddv[d] = static_cast<char*>(dv ? dv[d] : nullptr);
   }
   const size_t bq = TT * H * 256, bk = TT * G * 256;
+  join_caller();  // d_o is produced on the caller's stream
   for (int d = 0; d < R_; ++d) {
     DevState& D = dev_[d];
     D.next_event = 0;
     D.next_kev = 0;
+    D.next_tev = 0;
     D.launches = 0;
     if (!local(d)) continue;
     DeviceGuard gd(D.ordinal);
-    if (opt.timing) CUDA_OK(cudaEventRecord(D.t0, D.cs));
+    if (opt.timing || opt.trace) CUDA_OK(cudaEventRecord(D.t0, D.cs));
   }
   int slot = -1;
   if (host) {
@@ -428,7 +458,6 @@ void Executor::backward(const void* const* d_o, void* const* dq, void* const* dk
           p.slot_rows = static_cast<int32_t>(D.slot_rows);
           p.scale_log2 = static_cast<float>(1.4426950408889634) * scale;
           p.scale = scale;
-          p.debug_flags = opt.bwd_debug;
           std::pair<cudaEvent_t, cudaEvent_t> ke{};
           if (opt.kernel_timing) { ke = kernel_events(d); CUDA_OK(cudaEventRecord(ke.first, D.cs)); }
           launch_attn_bwd(D.tm_q64, D.tm_do, D.tm_kv, D.tm_dq, D.tm_dkv, p, attn_grid(d, op.bgrid), D.cs);
@@ -531,10 +560,12 @@ void Executor::backward(const void* const* d_o, void* const* dq, void* const* dk
     if (fr.empty()) fr.push_back(staging_event(0));
     CUDA_OK(cudaEventRecord(fr[0], d2h_));
   }
+  release_caller();  // dq / dk / dv (device buffers) are ready in the caller's stream order
   fill_report(rep, true);
 }
 
 void Executor::synchronize() {
+  if (host_only_) return;
   for (auto& D : dev_) {
     DeviceGuard gd(D.ordinal);
     CUDA_OK(cudaStreamSynchronize(D.cs));

@@ -27,12 +27,13 @@ LIB_PATH = os.environ.get("DCPX_LIB") or os.path.join(_HERE, "libdcpx.so")
 STATUS = {0: "OK", 1: "Error", 2: "DeadlockError", 3: "TagMismatchError", 4: "BufferOverflowError",
           5: "InfeasibleError", 6: "CudaError", 7: "Unsupported"}
 
-# Every symbol include/dcpx.h declares (checked by tests/test_capi_symbols.py).
+# Every symbol include/dcpx.h declares (checked by tests/test_boundary_cpu.py).
 EXPORTS = ["dcpx_create", "dcpx_create_rank", "dcpx_rank_export", "dcpx_rank_connect", "dcpx_prepare",
            "dcpx_load_inputs", "dcpx_load_inputs_host", "dcpx_forward", "dcpx_forward_host",
            "dcpx_backward", "dcpx_backward_host", "dcpx_load_inputs_dev", "dcpx_forward_dev",
-           "dcpx_backward_dev", "dcpx_synchronize", "dcpx_debug_arena",
-           "dcpx_set_option", "dcpx_trace", "dcpx_last_error", "dcpx_version", "dcpx_destroy"]
+           "dcpx_backward_dev", "dcpx_synchronize", "dcpx_set_streams", "dcpx_check_plans",
+           "dcpx_debug_arena", "dcpx_set_option", "dcpx_trace", "dcpx_last_error", "dcpx_version",
+           "dcpx_destroy"]
 
 
 class DCPXError(RuntimeError):
@@ -57,8 +58,11 @@ def lib():
                      "dcpx_load_inputs", "dcpx_load_inputs_host", "dcpx_forward",
                      "dcpx_forward_host", "dcpx_backward", "dcpx_backward_host",
                      "dcpx_load_inputs_dev", "dcpx_forward_dev", "dcpx_backward_dev",
-                     "dcpx_synchronize", "dcpx_debug_arena", "dcpx_set_option"):
+                     "dcpx_synchronize", "dcpx_debug_arena", "dcpx_set_option", "dcpx_set_streams",
+                     "dcpx_check_plans"):
             getattr(L, name).restype = C.c_int
+        L.dcpx_set_streams.argtypes = [C.c_void_p, C.c_int, C.c_void_p]
+        L.dcpx_check_plans.argtypes = [C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_char_p, C.c_int64]
         L.dcpx_create.argtypes = [C.c_int, C.POINTER(C.c_int), C.c_int, C.POINTER(C.c_void_p)]
         L.dcpx_create_rank.argtypes = [C.c_int, C.c_int, C.c_int, C.POINTER(C.c_void_p)]
         L.dcpx_rank_export.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.POINTER(C.c_int64)]
@@ -92,7 +96,10 @@ def _report_dict(r: P.c_report) -> dict:
                 total_flops=int(r.total_flops), per_device_send=[int(x) for x in r.per_device_send[:n]],
                 per_device_recv=[int(x) for x in r.per_device_recv[:n]], wire_bytes=int(r.wire_bytes),
                 makespan=r.makespan, device_ms=r.device_ms, kernel_launches=r.kernel_launches,
-                attn_launches=r.attn_launches, attn_ms=r.attn_ms, attn_ms_sum=r.attn_ms_sum)
+                attn_launches=r.attn_launches, attn_ms=r.attn_ms, attn_ms_sum=r.attn_ms_sum,
+                wire_per_device_send=[int(x) for x in r.wire_per_device_send[:n]],
+                wire_per_device_recv=[int(x) for x in r.wire_per_device_recv[:n]],
+                units=int(r.units), windowed=int(r.windowed))
 
 
 def _ptr(t) -> Optional[int]:
@@ -127,12 +134,14 @@ class DCPExecutor:
         if rank is not None:
             self._check(lib().dcpx_create_rank(rank, world, cuda_ordinal, C.byref(self._h)), create=True)
             self.ndev = world
+            self.ordinals = [cuda_ordinal] * world
         else:
             devices = list(devices or [0])
             arr = (C.c_int * len(devices))(*devices)
             tr = {"local": 0, "p2p": 0, "nccl": 1}[transport]  # dcpx_transport
             self._check(lib().dcpx_create(len(devices), arr, tr, C.byref(self._h)), create=True)
             self.ndev = len(devices)
+            self.ordinals = devices
         self.bundle: Optional[P.PlanBundle] = None
         self._keep = None
 
@@ -180,9 +189,18 @@ class DCPExecutor:
         self._check(lib().dcpx_rank_connect(self._h, allb, size.value))
         dist.barrier()  # every rank mapped every arena before anyone runs
 
+    def _streams(self):
+        """Orders the next call after torch's current stream on every plan device's GPU and
+        makes that stream wait for the call (dcpx.h stream contract)."""
+        import torch
+        cur = {o: torch.cuda.current_stream(o).cuda_stream for o in set(self.ordinals)}
+        arr = (C.c_void_p * self.ndev)(*[cur[o] for o in self.ordinals])
+        self._check(lib().dcpx_set_streams(self._h, self.ndev, arr))
+
     # Tensors, or lists with one tensor per plan device in that device's own memory
     # (the distributed layout: dcpx_*_dev; device d touches only the rows it owns).
     def load_inputs(self, q, k, v):
+        self._streams()
         if isinstance(q, (list, tuple)):
             self._check(lib().dcpx_load_inputs_dev(self._h, _ptrs(q), _ptrs(k), _ptrs(v)))
         elif q.is_cuda:
@@ -191,6 +209,7 @@ class DCPExecutor:
             self._check(lib().dcpx_load_inputs_host(self._h, _ptr(q), _ptr(k), _ptr(v)))
 
     def forward(self, o=None, lse=None, host: bool = False) -> dict:
+        self._streams()
         rep = P.c_report()
         if isinstance(o, (list, tuple)) or isinstance(lse, (list, tuple)):
             self._check(lib().dcpx_forward_dev(self._h, _ptrs(o), _ptrs(lse), C.byref(rep)))
@@ -200,6 +219,7 @@ class DCPExecutor:
         return _report_dict(rep)
 
     def backward(self, d_o, dq, dk, dv, host: bool = False) -> dict:
+        self._streams()
         rep = P.c_report()
         if isinstance(d_o, (list, tuple)):
             self._check(lib().dcpx_backward_dev(self._h, _ptrs(d_o), _ptrs(dq), _ptrs(dk), _ptrs(dv),
@@ -226,6 +246,32 @@ class DCPExecutor:
         ptr, rows = C.c_void_p(), C.c_int64()
         self._check(lib().dcpx_debug_arena(self._h, dev, kind, C.byref(ptr), C.byref(rows)))
         return ptr.value, rows.value
+
+    def arena_view(self, dev: int, kind: int, slots: int):
+        """torch view (no copy) of the first `slots` slots of an arena of plan device `dev`:
+        kind 0 Q / 2 O -> bf16 [slots, slot_rows, 128]; 1 KV -> bf16 [slots, 2, slot_rows, 128];
+        3 LSE -> fp32 [slots, slot_rows] (natural log). Introspection (dcpx_debug_arena)."""
+        import torch
+        ptr, rows = self.arena(dev, kind)
+        shape = {0: (slots, rows, 128), 1: (slots, 2, rows, 128), 2: (slots, rows, 128), 3: (slots, rows)}[kind]
+
+        class _CAI:
+            __cuda_array_interface__ = {"shape": shape, "typestr": "<f4" if kind == 3 else "<i2",
+                                        "data": (ptr, False), "version": 3}
+        t = torch.as_tensor(_CAI(), device=f"cuda:{self.ordinals[dev]}")
+        return t if kind == 3 else t.view(torch.bfloat16)
+
+
+def check_plans(bundle: P.PlanBundle) -> None:
+    """Host-only verification of a bundle's plans (dcpx_check_plans: verify_plans plus the
+    lockstep deadlock / tag replay); raises DCPXError with the reference's exception kind.
+    Needs no GPU."""
+    keep, g, m, pv = bundle.c_views()
+    err = C.create_string_buffer(4096)
+    rc = lib().dcpx_check_plans(len(pv), pv, C.byref(g), C.byref(m), err, 4096)
+    del keep
+    if rc != 0:
+        raise DCPXError(rc, err.value.decode())
 
 
 def run(bundle: P.PlanBundle, q, k, v, devices: Optional[Sequence[int]] = None):

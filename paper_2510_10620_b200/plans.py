@@ -77,7 +77,9 @@ class c_report(C.Structure):
                 ("per_device_recv", C.c_uint64 * 64), ("wire_bytes", C.c_uint64),
                 ("makespan", C.c_double), ("device_ms", C.c_double),
                 ("kernel_launches", C.c_int32), ("attn_launches", C.c_int32),
-                ("attn_ms", C.c_double), ("attn_ms_sum", C.c_double)]
+                ("attn_ms", C.c_double), ("attn_ms_sum", C.c_double),
+                ("wire_per_device_send", C.c_uint64 * 64), ("wire_per_device_recv", C.c_uint64 * 64),
+                ("units", C.c_int32), ("windowed", C.c_int32)]
 
 
 def _ptr(a: np.ndarray) -> int:
@@ -171,6 +173,68 @@ class PlanBundle:
                         send[src] += size; recv[dst] += size
                         send[dst] += size; recv[src] += size
         return send, recv
+
+    def wire_bytes(self):
+        """Bytes the executor's transfers actually move, per device (forward and backward):
+        forward O blocks travel with their fp32 LSE (4 B/row); backward Q fetches move Q, dO
+        and the fp32 LSE and Delta rows (8 B/row); gradient returns are fp32 (2x the planned
+        block bytes). Returns ((fwd_send, fwd_recv), (bwd_send, bwd_recv)), uint64[R] each."""
+        fs, fr, bs, br = (np.zeros(self.R, np.uint64) for _ in range(4))
+        db = self.data_blocks
+        for dp in self.devices:
+            for ins in dp.instructions():
+                if ins["op"] != OP_COMM_LAUNCH or ins["send"]:
+                    continue
+                src, dst = ins["peer"], dp.device
+                for b in dp.blocks[ins["offset"]: ins["offset"] + ins["count"]]["block"]:
+                    kind = int(db["kind"][b])
+                    size = int(db["size_bytes"][b])
+                    rows = int(db["tok_end"][b] - db["tok_begin"][b])
+                    fwd = size + (4 * rows if kind == KIND_O else 0)
+                    fs[src] += fwd; fr[dst] += fwd
+                    if kind == KIND_Q:
+                        out = 2 * size + 8 * rows
+                        bs[src] += out; br[dst] += out
+                        bs[dst] += 2 * size; br[src] += 2 * size
+                    elif kind == KIND_KV:
+                        bs[src] += size; br[dst] += size
+                        bs[dst] += 2 * size; br[src] += 2 * size
+        return (fs, fr), (bs, br)
+
+    def item_sample(self, items: np.ndarray) -> "PlanBundle":
+        """A one-device bundle executing each of `items` (ATT_ITEM rows taken from any of this
+        bundle's plans) on its own: their Q / KV blocks resident, one AttentionInstr, item i
+        writing O slot i, no reductions. After a forward, O-arena slot i holds item i's
+        normalised partial and the LSE arena its m + ln l -- exactly what exec_attention
+        (simexec.hpp:33-76) returns for that item, so a sample of the plan's items can be
+        compared one by one with the reference executor (bench.py's cpu_baseline leg)."""
+        cb = self.comp_blocks
+        qb = [int(cb["q_block"][int(c)]) for c in items["comp_id"]]
+        kb = [int(cb["kv_block"][int(c)]) for c in items["comp_id"]]
+        uq = {b: i for i, b in enumerate(dict.fromkeys(qb))}
+        uk = {b: i for i, b in enumerate(dict.fromkeys(kb))}
+        its = np.array(items, ATT_ITEM).copy()
+        rows = []
+        for i in range(len(its)):
+            its["q_slot"][i], its["kv_slot"][i], its["out_slot"][i] = uq[qb[i]], uk[kb[i]], i
+            if its["rows_offset"][i] >= 0:
+                raise ValueError("item_sample: items with explicit rows are not supported")
+        res_q = np.array([(b, s) for b, s in uq.items()], BLOCK_SLOT)
+        res_kv = np.array([(b, s) for b, s in uk.items()], BLOCK_SLOT)
+        dp = DevicePlan(device=0, divisions=1, capacity=np.array([len(uq), len(uk), len(its)], np.int32),
+                        resident_q=res_q, resident_kv=res_kv, resident_o=np.zeros(0, BLOCK_SLOT),
+                        instr=np.array([[OP_ATTENTION, 0, 0, 0, 0, len(its), 0, -1]], np.int32),
+                        items=its, srcs=np.zeros(0, np.int32), copies=np.zeros(0, COPY_ITEM),
+                        blocks=np.zeros(0, BLOCK_SLOT), tags=[])
+        z = np.zeros(1, np.uint64)
+        return PlanBundle(R=1, T=1, H=self.H, G=self.G, D=self.D, bpe=self.bpe,
+                          seq_lengths=self.seq_lengths, block_sizes=self.block_sizes,
+                          seq_offsets=self.seq_offsets, ranges=self.ranges, data_blocks=self.data_blocks,
+                          comp_blocks=self.comp_blocks,
+                          data_block_device=np.zeros(len(self.data_blocks), np.int32),
+                          comp_block_device=np.zeros(len(self.comp_blocks), np.int32),
+                          dev_flops=z, per_device_send=z, per_device_recv=z.copy(),
+                          volume=np.zeros(5, np.uint64), devices=[dp], meta={"item_sample": str(len(its))})
 
     # ---- persistence -------------------------------------------------------------
     def save(self, path: str) -> None:

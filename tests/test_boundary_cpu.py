@@ -109,3 +109,100 @@ def test_cached_configs_present():
         assert os.path.exists(path), name
     b = P.PlanBundle.load(os.path.join(REPO, "plans", "cfg1_R2.npz"))
     assert int(b.volume[0]) == 12582912 and len(b.comp_blocks) == 416  # SURVEY.md section 6 probe
+
+
+def test_check_plans_host_only():
+    """dcpx_check_plans: verify_plans + the lockstep replay without a GPU. A planner bundle
+    passes; deleting a device's sends is a deadlock (tests/test_simexec.cpp:251-270); a
+    renamed receive tag is a tag mismatch; an out-of-range slot is a buffer overflow
+    (plan.hpp:368-380)."""
+    specs = [PL.SeqSpec(256)]
+    b = PL.Batch.from_specs(specs, 1, 1, 128)
+    gt, cq = b.graph_counts(128)
+
+    def fresh():
+        return PL.plan(b, 2, 128, placement="explicit", group_dev=gt, comp_dev=cq, divisions=2)
+
+    E.check_plans(fresh())  # no exception
+    bad = fresh()
+    dp = bad.devices[0]
+    dp.instr = dp.instr[[i for i, r in enumerate(dp.instr) if not (r[0] == 3 and r[2] == 1)]]
+    with pytest.raises(E.DCPXError) as ei:
+        E.check_plans(bad)
+    assert ei.value.kind == "DeadlockError"
+
+    bad = fresh()
+    dp = bad.devices[1]
+    waits = [i for i, r in enumerate(dp.instr) if r[0] == 4]
+    assert waits
+    dp.tags = list(dp.tags) + ["no-such-tag"]  # the wait names a tag no receive posted
+    dp.instr = dp.instr.copy()
+    dp.instr[waits[0], 7] = len(dp.tags) - 1
+    with pytest.raises(E.DCPXError) as ei:
+        E.check_plans(bad)
+    assert ei.value.kind == "TagMismatchError"
+
+    bad = fresh()
+    dp = bad.devices[0]
+    att = [i for i, r in enumerate(dp.instr) if r[0] == 0]
+    dp.items = dp.items.copy()
+    dp.items["out_slot"][int(dp.instr[att[0]][6])] = int(dp.capacity[2]) + 5
+    with pytest.raises(E.DCPXError) as ei:
+        E.check_plans(bad)
+    assert ei.value.kind == "BufferOverflowError"
+
+
+def test_check_plans_any_head_dim():
+    """The host-only check executes nothing, so it accepts shapes the sm_100a kernels do not
+    (head_dim 64): the cost-only drop-in path (include/dcp_gpu.hpp) relies on this."""
+    b = PL.Batch.from_specs([PL.SeqSpec(300), PL.SeqSpec(100, "lambda", sink=4, window=20)], 2, 1, 64)
+    bundle = PL.plan(b, 2, 128, eps_intra=0.5, eps_data=0.6)
+    E.check_plans(bundle)
+
+
+def test_dropin_cost_only_without_gpu():
+    """include/dcp_gpu.hpp in cost-only mode (SimOptions::numeric = false) runs without a GPU
+    and equals the reference's cost-mode run() report for D = 64, raising DeadlockError where
+    the reference does (tests/cpp/test_dcp_gpu_cost.cpp)."""
+    binp = os.path.join(REPO, "tests", "cpp", "_build", "test_dcp_gpu_cost")
+    if not os.path.exists(binp):
+        pytest.skip("drop-in test binaries are built where /root/reference exists (tools/build.py)")
+    r = subprocess.run([binp], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and "COST PASS" in r.stdout, r.stdout + r.stderr
+
+
+def test_item_sample_bundle_and_reference_items():
+    """bench.py's CPU-baseline check: PlanBundle.item_sample builds a valid one-device plan
+    running sampled AttentionItems alone (host-only check), and oracle.ref_run_items (the
+    reference exec_attention on given inputs) returns (out, m + ln l) equal to the C
+    restatement on the same items."""
+    import oracle as O
+    if not O.ref_available():
+        pytest.skip("reference shim not built")
+    specs = [PL.SeqSpec(700), PL.SeqSpec(500, "lambda", sink=16, window=100),
+             PL.SeqSpec(600, "shared_question", question_len=100, answer_lens=[250, 250])]
+    b = PL.Batch.from_specs(specs, 4, 2, 128)
+    bundle = PL.plan(b, 2, 256, eps_intra=0.4, eps_data=0.6)
+    items = np.concatenate([dp.items for dp in bundle.devices])[::3]
+    sb = bundle.item_sample(items)
+    E.check_plans(sb)
+    assert sb.devices[0].capacity[2] == len(items)
+    rng = np.random.default_rng(0)
+    T, H, G = bundle.total_tokens, bundle.H, bundle.G
+    q, k, v = (rng.standard_normal((T, n, 128)) for n in (H, G, G))
+    work = []
+    for it in items[:6]:
+        s, h = int(it["seq"]), int(it["head"])
+        off = int(bundle.seq_offsets[s])
+        rows = O.item_rows(bundle, s, int(it["q_begin"]), int(it["q_end"]), int(it["kv_begin"]), int(it["kv_end"]))
+        gq = h * G // H
+        work.append(dict(rows=rows, q=q[off + int(it["q_begin"]):off + int(it["q_end"]), h],
+                         k=k[off + int(it["kv_begin"]):off + int(it["kv_end"]), gq],
+                         v=v[off + int(it["kv_begin"]):off + int(it["kv_end"]), gq]))
+    outs, lses, sec = O.ref_run_items(work, 128, 2)
+    for w, o, l in zip(work, outs, lses):
+        o2, m2, l2 = O.exec_attention(w["q"], w["k"], w["v"], w["rows"])
+        assert np.abs(o - o2).max() <= 1e-12
+        fin = l2 > 0
+        assert np.array_equal(np.isfinite(l), fin)
+        assert np.abs(l[fin] - (m2[fin] + np.log(l2[fin]))).max() <= 1e-12

@@ -132,3 +132,105 @@ def test_fullsize_backward_plan_invariance(cfg):
     assert float((l4[fin] - l1[fin]).abs().max()) <= LSE_TOL
     for a, b in zip(g4, g1):
         assert _rel_dev(a, b) <= 1e-2
+
+
+def _ref_backward_slice(bundle, q, k, v, d_o, seq, key_lo, key_hi, group, chunk=512):
+    """FP64 on the GPU: dK / dV of keys [key_lo, key_hi) of sequence `seq`, kv group `group`,
+    and dQ of every q row that attends one of those keys (heads of the group), from the bf16
+    inputs. Each such row is processed whole (its LSE and Delta = dO . O need all its keys),
+    keys gathered per chunk of rows from the union of the rows' <= 2 attend ranges.
+    Returns (rows, heads, dq [rows, heads, D], dk [keys, D], dv [keys, D]) with sequence-local
+    row / key indices."""
+    import torch
+    H, G = bundle.H, bundle.G
+    off = int(bundle.seq_offsets[seq])
+    L = int(bundle.seq_offsets[seq + 1]) - off
+    rg = np.asarray(bundle.ranges[off:off + L], np.int64)
+    hit0 = (rg[:, 1] > rg[:, 0]) & (rg[:, 0] < key_hi) & (rg[:, 1] > key_lo)
+    hit1 = (rg[:, 3] > rg[:, 2]) & (rg[:, 2] < key_hi) & (rg[:, 3] > key_lo)
+    rows = np.nonzero(hit0 | hit1)[0]
+    heads = [h for h in range(H) if h * G // H == group]
+    scale = 1.0 / np.sqrt(128.0)
+    kk = k[off:off + L, group].double()
+    vv = v[off:off + L, group].double()
+    nk = key_hi - key_lo
+    dk = torch.zeros((nk, 128), dtype=torch.float64, device="cuda")
+    dv = torch.zeros_like(dk)
+    dq = torch.zeros((len(rows), len(heads), 128), dtype=torch.float64, device="cuda")
+    for c0 in range(0, len(rows), chunk):
+        r = rows[c0:c0 + chunk]
+        iv = []  # union of the chunk rows' ranges as merged intervals
+        for b, e in sorted({(int(x), int(y)) for x, y in np.concatenate([rg[r][:, 0:2], rg[r][:, 2:4]]) if y > x}):
+            if iv and b <= iv[-1][1]:
+                iv[-1][1] = max(iv[-1][1], e)
+            else:
+                iv.append([b, e])
+        keys = np.concatenate([np.arange(b, e) for b, e in iv])
+        kt = torch.from_numpy(keys).cuda()
+        rr = torch.from_numpy(rg[r]).cuda()
+        mask = ((kt[None, :] >= rr[:, 0:1]) & (kt[None, :] < rr[:, 1:2])) | \
+               ((kt[None, :] >= rr[:, 2:3]) & (kt[None, :] < rr[:, 3:4]))
+        Kc, Vc = kk[kt], vv[kt]
+        sel = (kt >= key_lo) & (kt < key_hi)
+        for hi, h in enumerate(heads):
+            rows_t = torch.from_numpy(off + r).cuda()
+            Q, dO = q[rows_t, h].double(), d_o[rows_t, h].double()
+            S = (Q @ Kc.T) * scale
+            S = torch.where(mask, S, torch.full_like(S, float("-inf")))
+            lse = torch.logsumexp(S, 1, keepdim=True)
+            P = torch.where(mask, torch.exp(S - torch.where(torch.isfinite(lse), lse, torch.zeros_like(lse))),
+                            torch.zeros_like(S))
+            O = P @ Vc
+            delta = (dO * O).sum(1, keepdim=True)
+            dS = P * (dO @ Vc.T - delta)
+            dq[c0:c0 + len(r), hi] = scale * (dS @ Kc)
+            dk.index_add_(0, kt[sel] - key_lo, scale * (dS[:, sel].T @ Q))
+            dv.index_add_(0, kt[sel] - key_lo, P[:, sel].T @ dO)
+    return rows, heads, dq, dk, dv
+
+
+# (config, [(sequence, key_lo, key_hi)]): whole short sequences plus a key range of a long
+# one (causal: its last keys; lambda: keys mid-sequence whose rows reach back to the sink,
+# and the sink keys themselves, read by every row of their sequence)
+BWD_SLICES = {
+    "cfg2_R1": [(0, 0, 6949), (4, 21000, 22616)],
+    "cfg3_R1": [(2, 0, 4462), (3, 40000, 41536), (4, 0, 128)],
+    "cfg4_sq_B2048_R1": [(2, 0, 4462), (4, 0, 6949)],
+}
+
+
+@pytest.mark.parametrize("name", list(BWD_SLICES))
+def test_fullsize_backward_vs_fp64(name):
+    """The production backward (windowed, merged-head units at the default options) at full
+    size against FP64: dQ of every row attending the checked keys, dK / dV of those keys, for
+    one kv group per slice (max |x - ref| / max |ref| <= 2e-2 per tensor)."""
+    import torch
+
+    from make_plans import load
+    bundle = load(name)
+    q, k, v, d_o = _inputs(bundle, seed=11)
+    from paper_2510_10620_b200.executor import DCPExecutor
+    ex = DCPExecutor([0])
+    ex.prepare(bundle)
+    T, H, G = bundle.total_tokens, bundle.H, bundle.G
+    o = torch.zeros((T, H, 128), dtype=torch.bfloat16, device="cuda")
+    lse = torch.zeros((H, T), device="cuda")
+    dq, dk, dv = torch.zeros_like(q), torch.zeros_like(k), torch.zeros_like(v)
+    ex.load_inputs(q, k, v)
+    ex.forward(o, lse)
+    rep = ex.backward(d_o, dq, dk, dv)
+    ex.synchronize()
+    ex.close()
+    if name != "cfg4_sq_B2048_R1":
+        assert rep["windowed"] > 0  # the q-windowed unit path every long-unit config runs
+    for i, (s, lo, hi) in enumerate(BWD_SLICES[name]):
+        grp = (3 * i + 1) % G
+        rows, heads, rq, rk, rv = _ref_backward_slice(bundle, q, k, v, d_o, s, lo, hi, grp)
+        off = int(bundle.seq_offsets[s])
+        rt = torch.from_numpy(off + rows).cuda()
+        got_q = dq[rt][:, heads].double()
+        got_k = dk[off + lo:off + hi, grp].double()
+        got_v = dv[off + lo:off + hi, grp].double()
+        for what, a, b in (("dq", got_q, rq), ("dk", got_k, rk), ("dv", got_v, rv)):
+            err = float((a - b).abs().max() / b.abs().max().clamp_min(1e-30))
+            assert err <= O_TOL, (name, s, lo, hi, what, err)

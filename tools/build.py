@@ -102,7 +102,8 @@ def build_dropin_test(force=False):
     pipeline_run; both compiled against the unchanged reference headers."""
     lib = os.path.join(REPO, "paper_2510_10620_b200", "libdcpx.so")
     out = None
-    for name, hdr in (("test_dcp_gpu_run", "dcp_gpu.hpp"), ("test_gpu_pipeline", "dcp_gpu_pipeline.hpp")):
+    for name, hdr in (("test_dcp_gpu_run", "dcp_gpu.hpp"), ("test_gpu_pipeline", "dcp_gpu_pipeline.hpp"),
+                      ("test_dcp_gpu_cost", "dcp_gpu.hpp")):
         src = os.path.join(REPO, "tests", "cpp", name + ".cpp")
         out = os.path.join(REPO, "tests", "cpp", "_build", name)
         if not os.path.isdir(os.path.join(REF, "include", "dcp")):
@@ -114,13 +115,6 @@ def build_dropin_test(force=False):
             _run(["g++", "-std=c++20", "-O2", f"-I{REF}/include", f"-I{REF}/tests", f"-I{REPO}/include",
                   "-I/usr/local/cuda/include", src, "-o", out, lib, "-L/usr/local/cuda/lib64", "-lcudart",
                   "-Wl,-rpath,$ORIGIN/../../../paper_2510_10620_b200", "-pthread"])
-    return out
-    deps = [src, lib, os.path.join(REPO, "include", "dcp_gpu.hpp"), os.path.join(REPO, "include", "dcpx.h")]
-    if force or _stale(out, deps):
-        os.makedirs(os.path.dirname(out), exist_ok=True)
-        _run(["g++", "-std=c++20", "-O2", f"-I{REF}/include", f"-I{REF}/tests", f"-I{REPO}/include",
-              "-I/usr/local/cuda/include", src, "-o", out, lib, "-L/usr/local/cuda/lib64", "-lcudart",
-              "-Wl,-rpath,$ORIGIN/../../../paper_2510_10620_b200", "-pthread"])
     return out
 
 
