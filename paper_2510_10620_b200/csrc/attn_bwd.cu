@@ -18,7 +18,7 @@
 //   warp 0      TMA producer: Q, dO tiles + LSE/Delta rows per step (3 stages)
 //   warp 1      TMEM owner + tcgen05.mma issuer
 //   warp 2      TMA producer: K, V per unit
-//   warp 3      idle (register donor)
+//   warp 3      unit scheduler (dynamic: global counter -> shared ring, see sched_produce)
 //   warps 4-7   compute group 0 (even steps), warps 8-11 compute group 1 (odd steps):
 //               TMEM lane = kv row; P^T (bf16) -> TMEM, dS^T -> smem (SW128). The group
 //               taking a unit's first step first copies the unit's K tile into TMEM.
@@ -51,7 +51,7 @@ constexpr int kBwdStages = 3;
 // LSE[3] 1K | Delta[3] 1K | barriers
 constexpr int kBwdStageBytes = 32768;
 constexpr int kBwdSmemMain = (96 + 32 * kBwdStages + 32) * 1024;
-constexpr int kBwdSmem = kBwdSmemMain + 2048 + 256;
+constexpr int kBwdSmem = kBwdSmemMain + 2048 + 512;
 static_assert(kBwdSmem <= 232448, "backward shared memory exceeds the sm_100 opt-in limit");
 
 struct BwdBarriers {
@@ -60,9 +60,11 @@ struct BwdBarriers {
   uint64_t s_full[2], p_ready[2], dq_full[2], dq_empty[2], ds_free[2];
   uint64_t acc_full, acc_empty;
   uint64_t ktm_full, dp_free;
+  SchedRing sched;  // unit indices from the dynamic scheduler (warp 3)
   uint32_t tmem_base;
   uint32_t kv_seq;  // units whose K / V the MMA warp has seen land (monotonic)
 };
+static_assert(sizeof(BwdBarriers) <= 512, "barrier block exceeds its shared-memory reserve");
 
 // fp32 vector reduce-add into global memory (accumulators are shared with other CTAs
 // and with peer devices' gradient returns, so every update is atomic).
@@ -158,6 +160,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     mbar_init(&bars.ktm_full, 128);   // compute group of the unit's first step: K in TMEM
     mbar_init(&bars.dp_free, 128);    // compute group of step g: dP^T(g) loaded
     bars.kv_seq = 0;
+    sched_init(bars.sched, 15);  // consumers: warps 0-2, 8 compute warps, 4 drain warps
     fence_barrier_init();
     tma_prefetch_desc(&tm_q);
     tma_prefetch_desc(&tm_do);
@@ -178,7 +181,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     {
       BWD_PROF_DECL
       uint32_t g = 0;
-      for (int u = blockIdx.x; u < p.num_units; u += gridDim.x) {
+      for (uint32_t sk = 0;;) {
+        const int u = sched_next(bars.sched, sk);
+        if (u < 0) break;
         const BwdUnit U = p.units[u];
         for (int j = 0; j < U.step_count; ++j, ++g) {
           const BwdStep S = p.steps[U.step_begin + j];
@@ -206,7 +211,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     {
       BWD_PROF_DECL
       uint32_t it = 0;
-      for (int u = blockIdx.x; u < p.num_units; u += gridDim.x, ++it) {
+      for (uint32_t sk = 0;; ++it) {
+        const int u = sched_next(bars.sched, sk);
+        if (u < 0) break;
         const int32_t kv_row0 = p.units[u].kv_row0;
         BWD_TIMED(0, mbar_wait(&bars.kv_empty, (it & 1) ^ 1));
         if (elect_one()) {
@@ -268,7 +275,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         __syncwarp();
       };
       uint32_t g = 0, it = 0;
-      for (int u = blockIdx.x; u < p.num_units; u += gridDim.x, ++it) {
+      for (uint32_t sk = 0;; ++it) {
+        const int u = sched_next(bars.sched, sk);
+        if (u < 0) break;
         const BwdUnit U = p.units[u];
         BWD_TIMED(4, mbar_wait(&bars.kv_full, it & 1));
         tc_fence_after();
@@ -319,6 +328,10 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       }
       if (lane == 0) BWD_PROF_PRINT("mma", "q_full", "dq_empty", "p_ready", "acc_empty", "kv+ktm_full", "dp_free");
     }
+  } else if (warp == 3) {
+    // ------------------------------------------------------------ unit scheduler
+    if (lane == 0) sched_produce(bars.sched, p.sched, p.sched_base, p.num_units);
+    __syncwarp();
   } else if (warp >= 4 && warp < 12) {
     // ------------------------------------------------------------ compute warpgroups
     asm volatile("setmaxnreg.inc.sync.aligned.u32 168;");
@@ -329,7 +342,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     uint8_t* my_row0 = sDS + j * 128;
     BWD_PROF_DECL
     uint32_t g = 0, it = 0;
-    for (int u = blockIdx.x; u < p.num_units; u += gridDim.x, ++it) {
+    for (uint32_t sk = 0;; ++it) {
+      const int u = sched_next(bars.sched, sk);
+      if (u < 0) break;
       const BwdUnit U = p.units[u];
       const bool kv_valid = j < U.n_kv;
       // descriptors of my next step are loaded a step ahead so their latency hides
@@ -479,7 +494,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     const uint32_t gran = (uint32_t)(lane >> 2), sub = (uint32_t)(lane & 3) * 4;
     BWD_PROF_DECL
     uint32_t g = 0, it = 0;
-    for (int u = blockIdx.x; u < p.num_units; u += gridDim.x, ++it) {
+    for (uint32_t sk = 0;; ++it) {
+      const int u = sched_next(bars.sched, sk);
+      if (u < 0) break;
       const BwdUnit U = p.units[u];
       for (int s = 0; s < U.step_count; ++s, ++g) {
         const int q_row0 = p.steps[U.step_begin + s].q_row0;

@@ -12,7 +12,8 @@
 // CTA = 384 threads (3 warpgroups), persistent over FwdUnits:
 //   warp 0      TMA producer: Q tiles (2 x 128 rows), K/V sub-tiles (2-stage ring)
 //   warp 1      TMEM owner + single-thread tcgen05.mma issuer
-//   warps 2-3   idle (warpgroup 0 donates registers: setmaxnreg 88)
+//   warp 2      unit scheduler (dynamic: global counter -> shared ring, see sched_produce)
+//   warp 3      idle (warpgroup 0 donates registers: setmaxnreg 88)
 //   warps 4-7   softmax / correction / epilogue for q tile 0 (warp w reads TMEM
 //               lanes 32*(w%4)..+31, so the four warps cover rows 0-127); 208 regs
 //   warps 8-11  same for q tile 1
@@ -68,6 +69,7 @@ struct FwdBarriers {
   uint64_t q_full, q_empty;
   uint64_t k_full[2], v_full[2], kv_empty[2];
   uint64_t s_full[2], p_half[2], p_ready[2], o_full[2], o_empty[2];
+  SchedRing sched;  // unit indices from the dynamic scheduler (warp 2)
   uint32_t tmem_base;
 };
 
@@ -112,6 +114,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       mbar_init(&bars.o_full[i], 1);
       mbar_init(&bars.o_empty[i], 128);
     }
+    sched_init(bars.sched, 10);  // consumers: TMA warp, MMA warp, 8 softmax warps
     fence_barrier_init();
     tma_prefetch_desc(&tm_q);
     tma_prefetch_desc(&tm_kv);
@@ -128,7 +131,9 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     // converged warp, one elected lane issues (keeps the TMA operands in uniform registers)
     {
       uint32_t g = 0, it = 0;
-      for (int u = blockIdx.x; u < p.num_units; u += gridDim.x, ++it) {
+      for (uint32_t sk = 0;; ++it) {
+        const int u = sched_next(bars.sched, sk);
+        if (u < 0) break;
         const FwdUnit U = p.units[u];
         const int ntiles = U.n_rows > kTileRows ? 2 : 1;
         mbar_wait(&bars.q_empty, (it & 1) ^ 1);
@@ -178,7 +183,9 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         }
         __syncwarp();
       };
-      for (int u = blockIdx.x; u < p.num_units; u += gridDim.x, ++it) {
+      for (uint32_t sk = 0;; ++it) {
+        const int u = sched_next(bars.sched, sk);
+        if (u < 0) break;
         const FwdUnit U = p.units[u];
         const FwdStep* steps = p.steps + U.step_begin;
         bool has[2] = {false, false};
@@ -260,6 +267,10 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           if (has[t]) ++cnt_o[t];
       }
     }
+  } else if (warp == 2) {
+    // ------------------------------------------------------------ unit scheduler
+    if (lane == 0) sched_produce(bars.sched, p.sched, p.sched_base, p.num_units);
+    __syncwarp();
   } else if (warp >= 4) {
     // ------------------------------------------------------------ softmax / epilogue
     asm volatile("setmaxnreg.inc.sync.aligned.u32 208;");
@@ -272,7 +283,9 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     long long fprof[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
     const long long fprof_t0 = clock64();
 #endif
-    for (int u = blockIdx.x; u < p.num_units; u += gridDim.x) {
+    for (uint32_t sk = 0;;) {
+      const int u = sched_next(bars.sched, sk);
+      if (u < 0) break;
       const FwdUnit U = p.units[u];
       if (t == 1 && U.n_rows <= kTileRows) continue;
       const FwdStep* steps = p.steps + U.step_begin;

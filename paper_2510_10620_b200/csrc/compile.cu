@@ -218,6 +218,9 @@ void Executor::compile_device(int d) {
     zero(D.kv, std::max<int64_t>(1, D.cap_kv) * 2 * SR * 256);
     zero(D.o, std::max<int64_t>(1, D.cap_o) * SR * 256);
     zero(D.lse, std::max<int64_t>(1, D.cap_o) * SR * 4);
+    D.sched_ctr = static_cast<uint32_t*>(alloc(d, 256));
+    if (own) CUDA_OK(cudaMemset(D.sched_ctr, 0, 256));
+    D.sched_base = 0;
     // backward arenas, parallel to the Q arena (dO, LSE*log2e, Delta, dQ accumulator)
     // and to the KV arena (dK / dV accumulators)
     const int64_t nq = std::max<int64_t>(1, D.cap_q), nkv = std::max<int64_t>(1, D.cap_kv);
@@ -354,7 +357,8 @@ void Executor::compile_device(int d) {
             unit_cost.push_back(cost * 1000 + U.n_rows);
           }
         }
-        // longest-processing-time-first order for the static round-robin schedule
+        // longest-processing-time-first order (the kernels take units in list order from a
+        // dynamic scheduler, so the longest start first)
         std::vector<size_t> order(units.size());
         std::iota(order.begin(), order.end(), 0);
         std::stable_sort(order.begin(), order.end(), [&](size_t a, size_t b) { return unit_cost[a] > unit_cost[b]; });

@@ -121,6 +121,10 @@ struct DevState {
   // `caller` (its inputs) and `caller` waits for the call's device work (its outputs)
   cudaStream_t caller = cudaStreamLegacy;
   cudaEvent_t ev_join = nullptr, ev_done = nullptr;
+  // dynamic unit scheduler of the attention kernels: a device counter that every launch
+  // advances by num_units + grid, and its host-side running value (sched_produce)
+  uint32_t* sched_ctr = nullptr;
+  uint32_t sched_base = 0;
   // backward units of the last prepare (diagnostics in the report)
   int32_t bwd_units = 0, bwd_windowed = 0;
 };

@@ -97,7 +97,9 @@ struct BwdParams {
   int32_t slot_rows;
   float scale_log2;
   float scale;
-  int32_t _pad0, _pad1;
+  uint32_t* sched;      // dynamic-scheduler counter of the device (see sched_produce)
+  uint32_t sched_base;  // its value at this launch
+  int32_t _pad0;
 };
 
 struct FwdParams {
@@ -110,7 +112,8 @@ struct FwdParams {
   int32_t num_units;
   int32_t slot_rows;
   float scale_log2;  // log2(e) / sqrt(D)
-  int32_t _pad;
+  uint32_t sched_base;  // dynamic-scheduler counter value at this launch
+  uint32_t* sched;      // the device's scheduler counter (see sched_produce)
 };
 
 }  // namespace dcpx

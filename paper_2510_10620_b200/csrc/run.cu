@@ -146,8 +146,12 @@ void Executor::forward(void* const* o_out, float* const* lse_out, dcpx_report* r
         p.slot_rows = static_cast<int32_t>(D.slot_rows);
         p.scale_log2 = static_cast<float>(1.4426950408889634 / std::sqrt(static_cast<double>(g_.D)));
         std::pair<cudaEvent_t, cudaEvent_t> ke{};
+        const int grid = attn_grid(d, op.grid);
+        p.sched = D.sched_ctr;
+        p.sched_base = D.sched_base;
+        D.sched_base += static_cast<uint32_t>(op.num_units + grid);
         if (opt.kernel_timing) { ke = kernel_events(d); CUDA_OK(cudaEventRecord(ke.first, D.cs)); }
-        launch_attn_fwd(D.tm_q, D.tm_kv, p, attn_grid(d, op.grid), D.cs);
+        launch_attn_fwd(D.tm_q, D.tm_kv, p, grid, D.cs);
         if (opt.kernel_timing) CUDA_OK(cudaEventRecord(ke.second, D.cs));
         ++D.launches;
         break;
@@ -459,8 +463,12 @@ void Executor::backward(const void* const* d_o, void* const* dq, void* const* dk
           p.scale_log2 = static_cast<float>(1.4426950408889634) * scale;
           p.scale = scale;
           std::pair<cudaEvent_t, cudaEvent_t> ke{};
+          const int grid = attn_grid(d, op.bgrid);
+          p.sched = D.sched_ctr;
+          p.sched_base = D.sched_base;
+          D.sched_base += static_cast<uint32_t>(op.bnum_units + grid);
           if (opt.kernel_timing) { ke = kernel_events(d); CUDA_OK(cudaEventRecord(ke.first, D.cs)); }
-          launch_attn_bwd(D.tm_q64, D.tm_do, D.tm_kv, D.tm_dq, D.tm_dkv, p, attn_grid(d, op.bgrid), D.cs);
+          launch_attn_bwd(D.tm_q64, D.tm_do, D.tm_kv, D.tm_dq, D.tm_dkv, p, grid, D.cs);
           if (opt.kernel_timing) CUDA_OK(cudaEventRecord(ke.second, D.cs));
           ++D.launches;
         }

@@ -149,6 +149,53 @@ __device__ __forceinline__ uint32_t ld_acquire_cta(const uint32_t* p) {
   return v;
 }
 
+// ---- dynamic unit scheduler -------------------------------------------------------------
+// Persistent kernels take their work units from a global counter instead of a static
+// blockIdx-strided walk: one lane of a scheduler warp fetches unit indices (atomicAdd) into
+// a ring of shared-memory entries and every consumer warp reads the same sequence, so all
+// roles of a CTA agree on its units. CTAs then advance through the (host-ordered) unit list
+// together -- the units in flight at any time are ~gridDim.x consecutive ones, which keeps
+// the rows they share resident in L2 and removes the static schedule's tail imbalance.
+// The counter is never reset: every launch advances it by exactly num_units + gridDim.x
+// (each CTA's scheduler stops after its first fetch past the end), so the host passes the
+// launch's base value and keeps the running sum (modulo 2^32).
+constexpr int kSchedRing = 8;
+struct SchedRing {
+  uint64_t full[kSchedRing], empty[kSchedRing];
+  int32_t unit[kSchedRing];
+};
+
+__device__ __forceinline__ void sched_init(SchedRing& r, uint32_t consumer_warps) {
+  for (int i = 0; i < kSchedRing; ++i) {
+    mbar_init(&r.full[i], 1);
+    mbar_init(&r.empty[i], consumer_warps);
+  }
+}
+
+// Scheduler side (one thread). Writes -1 once the units are exhausted and returns.
+__device__ __forceinline__ void sched_produce(SchedRing& r, uint32_t* ctr, uint32_t base, int num_units) {
+  for (uint32_t k = 0;; ++k) {
+    const uint32_t s = k % kSchedRing;
+    mbar_wait(&r.empty[s], ((k / kSchedRing) & 1) ^ 1);
+    const uint32_t t = atomicAdd(ctr, 1u) - base;
+    const int u = t < static_cast<uint32_t>(num_units) ? static_cast<int>(t) : -1;
+    *reinterpret_cast<volatile int32_t*>(&r.unit[s]) = u;
+    mbar_arrive(&r.full[s]);  // release: the entry is visible to the waiters' acquire
+    if (u < 0) return;
+  }
+}
+
+// Consumer side (a converged warp): the next unit of this CTA, or -1 at the end.
+__device__ __forceinline__ int sched_next(SchedRing& r, uint32_t& k) {
+  const uint32_t s = k % kSchedRing;
+  mbar_wait(&r.full[s], (k / kSchedRing) & 1);
+  const int u = *reinterpret_cast<volatile int32_t*>(&r.unit[s]);
+  __syncwarp();
+  if ((threadIdx.x & 31) == 0) mbar_arrive(&r.empty[s]);
+  ++k;
+  return u;
+}
+
 // ---- TMA -----------------------------------------------------------------------------
 __device__ __forceinline__ void tma_prefetch_desc(const void* desc) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(desc) : "memory");
