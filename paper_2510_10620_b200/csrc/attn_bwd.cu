@@ -66,13 +66,9 @@ struct BwdBarriers {
 };
 static_assert(sizeof(BwdBarriers) <= 512, "barrier block exceeds its shared-memory reserve");
 
-// fp32 vector reduce-add into global memory (accumulators are shared with other CTAs
-// and with peer devices' gradient returns, so every update is atomic).
-__device__ __forceinline__ void red_add_v4(float* dst, const uint32_t* v) {
-  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst), "f"(__uint_as_float(v[0])),
-               "f"(__uint_as_float(v[1])), "f"(__uint_as_float(v[2])), "f"(__uint_as_float(v[3]))
-               : "memory");
-}
+// (Measured and not kept: dQ^T straight from registers into the accumulator with warp-wide
+// red.global.add.f32, skipping the shared-memory staging: cfg3 23.7 ms either way, cfg2
+// 21.9 vs 21.3 ms with the TMA bulk reduce-add.)
 
 // Bits [a, b) of a 32-bit word (a, b may lie outside [0, 32]).
 __device__ __forceinline__ uint32_t bits_in(int64_t a, int64_t b) {

@@ -43,7 +43,7 @@ class CfgC(C.Structure):
                 ("divisions", C.c_int32), ("max_slots_per_kind", C.c_int32),
                 ("block_size", C.c_int64), ("eps_inter", C.c_double), ("eps_intra", C.c_double),
                 ("eps_data", C.c_double), ("seed", C.c_uint64), ("verify", C.c_int32),
-                ("_pad", C.c_int32)]
+                ("threads", C.c_int32)]
 
 
 @dataclass
@@ -206,15 +206,19 @@ def plan(batch: Batch, devices: int, block_size: int, divisions: int = 4,
          eps_inter: float = 0.4, eps_intra: float = 0.1, eps_data: float = 0.05, seed: int = 0,
          machines: int = 1, placement: str = "dcp", group_dev: Optional[np.ndarray] = None,
          comp_dev: Optional[np.ndarray] = None, verify: bool = True,
-         max_slots_per_kind: int = 0, json_dir: Optional[str] = None) -> P.PlanBundle:
+         max_slots_per_kind: int = 0, json_dir: Optional[str] = None, threads: int = 0) -> P.PlanBundle:
     """Runs the reference planner (plan_batch, pipeline.hpp:29-38) and flattens it.
     json_dir: also write the plan in the reference's file formats there (batch.jsonl,
-    graph.json, placement.json, plan_d<d>.json, with the reference's own writers)."""
+    graph.json, placement.json, plan_d<d>.json, with the reference's own writers).
+    threads: 1 = the reference's single-threaded plan_batch, unchanged; 0 (all host cores) or
+    n > 1 = the same plan, bit for bit, with the partitioner's candidate evaluation and
+    repair scans on host threads (planner/dcp_partition_parallel.hpp)."""
     cfg = CfgC()
     cfg.machines, cfg.devices_per_machine = machines, devices // machines
     cfg.divisions, cfg.max_slots_per_kind, cfg.block_size = divisions, max_slots_per_kind, block_size
     cfg.eps_inter, cfg.eps_intra, cfg.eps_data, cfg.seed = eps_inter, eps_intra, eps_data, seed
     cfg.verify = 1 if verify else 0
+    cfg.threads = threads
     mode = {"dcp": 0, "ring": 1, "zigzag": 2, "explicit": 3}[placement]
     gd = np.ascontiguousarray(group_dev, np.int32) if group_dev is not None else None
     cd = np.ascontiguousarray(comp_dev, np.int32) if comp_dev is not None else None

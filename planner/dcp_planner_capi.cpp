@@ -25,6 +25,7 @@
 
 #include "dcp/baselines.hpp"
 #include "dcp/pipeline.hpp"
+#include "dcp_partition_parallel.hpp"
 #if __has_include(<json.hpp>)
 #include <filesystem>
 #include "dcp/io.hpp"  // the reference's plan / graph / placement JSON writers (io.hpp:72-352)
@@ -227,7 +228,8 @@ struct CfgC {
   int64_t block_size;
   double eps_inter, eps_intra, eps_data;
   uint64_t seed;
-  int32_t verify, _pad;
+  int32_t verify;
+  int32_t threads;  // 1: the reference plan_batch, unchanged; 0 (all cores) or > 1: plan_batch_parallel
 };
 
 dcp::DeviceTopology topo_of(const CfgC& c) {
@@ -344,8 +346,12 @@ int dcpp_plan(const dcpp_batch* b, const CfgC* cfg, int placement, const int32_t
     pc.placement.eps_data = cfg->eps_data;
     pc.placement.seed = cfg->seed;
     pc.compile.max_slots_per_kind = cfg->max_slots_per_kind;
-    if (placement == 0) {
+    if (placement == 0 && cfg->threads == 1) {
       p->pb = dcp::plan_batch(b->batch, topo, pc);  // pipeline.hpp:29-38, unchanged
+    } else if (placement == 0) {
+      // the same plan, bit for bit, with the partitioner's candidates and repair scans on
+      // host threads (planner/dcp_partition_parallel.hpp)
+      p->pb = dcpx_planner::plan_batch_parallel(b->batch, topo, pc, cfg->threads);
     } else {
       auto& pb = p->pb;
       pb.graph = dcp::generate_blocks(b->batch, pc.block_size);

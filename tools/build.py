@@ -80,10 +80,12 @@ def build_planner(force=False):
         if not os.path.exists(out):
             print("planner shim: reference sources absent and no prebuilt library", file=sys.stderr)
         return out
-    if force or _stale(out, [src, os.path.join(REPO, "include", "dcpx.h")]):
+    if force or _stale(out, [src, os.path.join(REPO, "include", "dcpx.h"),
+                             os.path.join(REPO, "planner", "dcp_partition_parallel.hpp")]):
         os.makedirs(os.path.dirname(out), exist_ok=True)
         nl = [f"-I{NLOHMANN}"] if os.path.exists(os.path.join(NLOHMANN, "json.hpp")) else []
-        _run(["g++", "-std=c++20", "-O3", "-fPIC", "-shared", f"-I{REF}/include", f"-I{REF}/tests", *nl,
+        _run(["g++", "-std=c++20", "-O3", "-fPIC", "-shared", f"-I{REF}/include", f"-I{REF}/tests",
+              f"-I{os.path.join(REPO, 'planner')}", *nl,
               src, "-o", out, "-pthread"])
     return out
 

@@ -47,7 +47,7 @@ CONFIGS = {
     "cfg1_R1": (cfg1_batch, 1, 1024, {}),
     "cfg1_R2": (cfg1_batch, 2, 1024, {}),
     # configs[1]: 8B-GPT layer (32/8 heads), causal, LongAlign-skewed 64K batch
-    # (synth seed 42, make_batches budget 65536, batch index 2: 6 sequences, 65,355 tokens)
+    # (synth seed 42, make_batches budget 65536, batch index 2: 6 sequences, 63,855 tokens)
     "cfg2_R1": (synth("causal", 65536, 65536, 2), 1, 1024, {}),
     "cfg2_R2": (synth("causal", 65536, 65536, 2), 2, 1024, {}),
     "cfg2_R4": (synth("causal", 65536, 65536, 2), 4, 1024, {}),
@@ -72,10 +72,15 @@ CONFIGS = {
     "cfg4_cb_B1024_R1": (synth("causal_blockwise", 131072, 131072, 0), 1, 1024, {}),
     "cfg4_cb_B2048_R1": (synth("causal_blockwise", 131072, 131072, 0), 1, 2048, {}),
     "cfg4_sq_B2048_R1": (synth("shared_question", 131072, 131072, 0), 1, 2048, {}),
-    # configs[4]: long-tail stress (512K + short tail), causal. Block 4096 plans in 40 s for
-    # one device but did not finish within 20 min for 4 or 8 devices (265,728 comp blocks),
-    # so the multi-device plans use block 8192 (68,096 comp blocks; R 4 plans in ~6 min).
+    # configs[4]: long-tail stress (512K + short tail), causal. With the reference's
+    # single-threaded partitioner block 4096 did not finish within 20 min for 4 or 8 devices
+    # (265,728 comp blocks), so block-8192 plans exist as well (68,096 comp blocks).
     "cfg5_R1": (cfg5_batch, 1, 4096, {}),
+    # block 4096 on 4 / 8 devices (265,728 comp blocks): unplannable by the single-threaded
+    # reference partitioner (> 20 min); the bit-identical parallel partitioner
+    # (planner/dcp_partition_parallel.hpp, planner.plan threads=0) plans them in minutes
+    "cfg5_R4": (cfg5_batch, 4, 4096, {}),
+    "cfg5_R8": (cfg5_batch, 8, 4096, {}),
     "cfg5_B8192_R1": (cfg5_batch, 1, 8192, {}),
     "cfg5_B8192_R4": (cfg5_batch, 4, 8192, {}),
     "cfg5_B8192_R8": (cfg5_batch, 8, 8192, {}),

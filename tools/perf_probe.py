@@ -23,6 +23,7 @@ def main():
     k = torch.randn((T, G, 128), device="cuda", generator=g).to(torch.bfloat16)
     v = torch.randn((T, G, 128), device="cuda", generator=g).to(torch.bfloat16)
     ex = DCPExecutor([0] * b.R)
+    ex.set_option("timing", 1)  # device_ms in the reports
     for opt in sys.argv[3:]:
         key, _, val = opt.partition("=")
         ex.set_option(key, int(val))

@@ -22,6 +22,7 @@ def main():
     k = torch.randn((T, G, 128), device="cuda").to(torch.bfloat16)
     v = torch.randn((T, G, 128), device="cuda").to(torch.bfloat16)
     ex = DCPExecutor([d % ng for d in range(b.R)])
+    ex.set_option("timing", 1)
     ex.prepare(b)
     o = torch.empty_like(q)
     lse = torch.empty((H, T), device="cuda")
