@@ -48,12 +48,13 @@ __global__ void __launch_bounds__(512, 1) bench(int iters, long long* out) {
     const uint32_t lane_addr = tbase + ((uint32_t)((warp & 3) * 32) << 16);
     const long long t0 = clock64();
     uint32_t acc = 0;
-    for (int i = 0; i < iters / 4; ++i) {
-      uint32_t r[32];
+    for (int i = 0; i < iters / 4; i += 2) {  // two loads in flight per warp
+      uint32_t r[32], r2[32];
       tmem_ld32(lane_addr + ((i * 32) & 255), r);
+      tmem_ld32(lane_addr + (((i + 1) * 32) & 255), r2);
       tmem_wait_ld();
 #pragma unroll
-      for (int e = 0; e < 32; ++e) acc += r[e];
+      for (int e = 0; e < 32; ++e) acc += r[e] ^ r2[e];
     }
     if (acc == 0x12345678u) out[1] = acc;
     const long long t = clock64() - t0;
