@@ -66,9 +66,13 @@ struct BwdBarriers {
 };
 static_assert(sizeof(BwdBarriers) <= 512, "barrier block exceeds its shared-memory reserve");
 
-// (Measured and not kept: dQ^T straight from registers into the accumulator with warp-wide
-// red.global.add.f32, skipping the shared-memory staging: cfg3 23.7 ms either way, cfg2
-// 21.9 vs 21.3 ms with the TMA bulk reduce-add.)
+// Measured limits (B200, cfg3 / cfg2, tools/perf_probe.py; profiles/r2_bwd_experiments.md):
+// two near-equal chains hold the kernel -- the dQ path (dQ^T MMA, drain, TMA reduce-add into
+// the fp32 accumulator, whose L2 read-modify-write plus the Q / dO loads keep L2 near its
+// throughput cap) and the MMA chain. Dropping the reduce alone: -7 %; dropping the dQ^T MMA
+// alone: 0 %; both: -21 %; skipping the exponentials: 0 %. Not kept: dQ^T straight from
+// registers by warp-wide red.global (no staging; equal or 3 % slower), rotating each unit's
+// steps so concurrent units reduce into different dQ rows (equal).
 
 // Bits [a, b) of a 32-bit word (a, b may lie outside [0, 32]).
 __device__ __forceinline__ uint32_t bits_in(int64_t a, int64_t b) {
