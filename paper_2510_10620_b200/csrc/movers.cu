@@ -231,6 +231,9 @@ __global__ void flag_wait_kernel(FlagList fl, int n, uint32_t epoch) {
       uint32_t v;
       asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(fl.f[i]) : "memory");
       if (static_cast<int32_t>(v - epoch) >= 0) break;
+#ifdef DCPX_JITTER
+      if (((clock64() >> 4) & 7) == 0) __nanosleep(3000);  // race-detection build: late pollers
+#endif
       __nanosleep(200);
       if (clock64() - t0 > 100000000000LL) __trap();  // ~50 s: a peer never arrived
     }

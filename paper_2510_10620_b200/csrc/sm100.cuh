@@ -120,7 +120,30 @@ __device__ __forceinline__ void watchdog_report(uint32_t* diag, uint32_t addr, u
 // ~10 s of waiting so a protocol bug surfaces as a launch error instead of a hung GPU.
 // Debug builds (-DDCPX_WATCHDOG_REPORT) also record the stuck barrier (watchdog_report)
 // before trapping; that path costs registers, so it is off in production builds.
+// Race-detection build (-DDCPX_JITTER, build/jitter/libdcpx.so; compute-sanitizer is closed
+// on this pool): every wait returns after a pseudo-random delay of up to ~2 us for about a
+// quarter of the calls, so each role's timing relative to the others is perturbed; a missing
+// or misplaced barrier then changes results (tests/test_gpu_jitter.py compares the outputs
+// with the product build's bit for bit where the computation is deterministic).
+#ifdef DCPX_JITTER
+__device__ __forceinline__ void jitter_point() {
+  uint32_t x = static_cast<uint32_t>(clock64()) * 2654435761u ^ ((threadIdx.x >> 5) * 40503u) ^ (blockIdx.x * 9973u);
+  x ^= x >> 13;
+  x *= 0x5bd1e995u;
+  x ^= x >> 15;
+  if ((x & 3u) == 0) __nanosleep(x & 2047u);
+}
+#else
+__device__ __forceinline__ void jitter_point() {}
+#endif
+
+__device__ __forceinline__ void mbar_wait_plain(uint64_t* bar, uint32_t parity);
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  mbar_wait_plain(bar, parity);
+  jitter_point();
+}
+
+__device__ __forceinline__ void mbar_wait_plain(uint64_t* bar, uint32_t parity) {
   const uint32_t addr = smem_u32(bar);
   if (mbar_try_wait(addr, parity)) return;
   const uint64_t t0 = global_ns();
@@ -190,6 +213,7 @@ __device__ __forceinline__ int sched_next(SchedRing& r, uint32_t& k) {
   const uint32_t s = k % kSchedRing;
   mbar_wait(&r.full[s], (k / kSchedRing) & 1);
   const int u = *reinterpret_cast<volatile int32_t*>(&r.unit[s]);
+  jitter_point();
   __syncwarp();
   if ((threadIdx.x & 31) == 0) mbar_arrive(&r.empty[s]);
   ++k;

@@ -35,7 +35,7 @@ def _run(cmd, cwd=REPO):
     subprocess.check_call(cmd, cwd=cwd)
 
 
-def build_dcpx(force=False):
+def build_dcpx(force=False, jitter=False):
     csrc = os.path.join(REPO, "paper_2510_10620_b200", "csrc")
     srcs = sorted(glob.glob(os.path.join(csrc, "*.cu")))
     deps = srcs + glob.glob(os.path.join(csrc, "*.h")) + glob.glob(os.path.join(csrc, "*.cuh")) + \
@@ -43,6 +43,8 @@ def build_dcpx(force=False):
     # instrumented variants build into build/<variant>/ (never over the product library)
     variant = "debug" if os.environ.get("DCPX_DEBUG") else "prof" if os.environ.get("DCPX_PROFILE") else \
         os.environ.get("DCPX_VARIANT", "")  # DCPX_VARIANT=name DCPX_DEFS="-DX=1 ..." for experiments
+    if jitter:
+        variant = "jitter"
     out = os.path.join(REPO, "build", variant, "libdcpx.so") if variant else \
         os.path.join(REPO, "paper_2510_10620_b200", "libdcpx.so")
     if not force and not _stale(out, deps):
@@ -57,8 +59,10 @@ def build_dcpx(force=False):
             extra = ["-DDCPX_WATCHDOG_REPORT"] if os.environ.get("DCPX_DEBUG") else []
             if os.environ.get("DCPX_PROFILE"):  # per-role wait-cycle counters printed by CTA 0
                 extra.append("-DDCPX_BWD_PROFILE")
-            if os.environ.get("DCPX_VARIANT"):
+            if os.environ.get("DCPX_VARIANT") and not jitter:
                 extra += os.environ.get("DCPX_DEFS", "").split()
+            if jitter:  # race-detection build (tests/test_gpu_jitter.py)
+                extra.append("-DDCPX_JITTER")
             _run([NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", f"-I{NCCL_DIR}/include",
                   "-Xptxas", "-warn-spills", *extra, "-c", s, "-o", o])
         objs.append(o)
@@ -124,6 +128,7 @@ def build_all(force=False):
     build_planner(force)
     build_oracle(force)
     out = build_dcpx(force)
+    build_dcpx(force, jitter=True)
     build_dropin_test(force)
     return out
 
