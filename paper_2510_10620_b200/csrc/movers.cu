@@ -62,7 +62,9 @@ __global__ void row_copy_kernel(const RowCopyJob* __restrict__ jobs, const int32
   }
 }
 
-// One warp per pair of rows: 16 lanes x 16 B cover one 128-wide bf16 row.
+// One warp per pair of rows: 16 lanes x 16 B cover one 128-wide bf16 row. Partials are taken
+// in groups of 4 whose LSE and O loads are all issued before any is used, so a thread keeps
+// four 16-byte loads in flight (the kernel is HBM / latency bound: ~(n_src + 1) x 260 B per row).
 __global__ void merge_kernel(const MergeJob* __restrict__ jobs, const int32_t* __restrict__ src_rows,
                              const int32_t* __restrict__ job_of_block, const int32_t* __restrict__ first_chunk,
                              __nv_bfloat16* o_arena, float* lse_arena) {
@@ -78,25 +80,37 @@ __global__ void merge_kernel(const MergeJob* __restrict__ jobs, const int32_t* _
 #pragma unroll
   for (int e = 0; e < 8; ++e) acc[e] = 0.f;
   float m = -CUDART_INF_F, denom = 0.f;
-  for (int i = 0; i < J.n_src; ++i) {
-    const int64_t row = (int64_t)src_rows[J.src_begin + i] + row_in_job;
-    const float l = lse_arena[row];
-    if (l == -CUDART_INF_F) continue;  // empty partial (l = 0 in the reference, :96-103)
-    if (l > m) {
-      const float c = __expf(m - l);  // m = -inf -> 0
-      denom *= c;
+  constexpr int kGroup = 4;
+  for (int i0 = 0; i0 < J.n_src; i0 += kGroup) {
+    float l[kGroup];
+    uint4 v[kGroup];
 #pragma unroll
-      for (int e = 0; e < 8; ++e) acc[e] *= c;
-      m = l;
+    for (int k = 0; k < kGroup; ++k) {
+      l[k] = -CUDART_INF_F;
+      if (i0 + k < J.n_src) {
+        const int64_t row = (int64_t)__ldg(src_rows + J.src_begin + i0 + k) + row_in_job;
+        l[k] = __ldcs(lse_arena + row);
+        v[k] = __ldcs(reinterpret_cast<const uint4*>(o_arena + row * 128) + sub);
+      }
     }
-    const float w = __expf(l - m);
-    denom += w;
-    const uint4 v = *(reinterpret_cast<const uint4*>(o_arena + row * 128) + sub);
-    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v);
 #pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      acc[2 * e] = fmaf(w, __bfloat162float(h[e].x), acc[2 * e]);
-      acc[2 * e + 1] = fmaf(w, __bfloat162float(h[e].y), acc[2 * e + 1]);
+    for (int k = 0; k < kGroup; ++k) {
+      if (l[k] == -CUDART_INF_F) continue;  // empty partial (l = 0 in the reference, :96-103)
+      if (l[k] > m) {
+        const float c = __expf(m - l[k]);  // m = -inf -> 0
+        denom *= c;
+#pragma unroll
+        for (int e = 0; e < 8; ++e) acc[e] *= c;
+        m = l[k];
+      }
+      const float w = __expf(l[k] - m);
+      denom += w;
+      const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v[k]);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        acc[2 * e] = fmaf(w, __bfloat162float(h[e].x), acc[2 * e]);
+        acc[2 * e + 1] = fmaf(w, __bfloat162float(h[e].y), acc[2 * e + 1]);
+      }
     }
   }
   float lse_out = -CUDART_INF_F;
