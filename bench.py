@@ -210,6 +210,28 @@ def cpu_baseline(bundle, q, k, v, seconds_target=15.0, check=True):
     return res
 
 
+def pcie_gbs(ordinal, nbytes=1 << 30):
+    """Pinned host <-> device copy bandwidth of this GPU's link, both directions running
+    concurrently (as in the e2e steps): (h2d GB/s, d2h GB/s)."""
+    import torch
+    hu = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
+    hd = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
+    du = torch.empty(nbytes, dtype=torch.uint8, device=f"cuda:{ordinal}")
+    dd = torch.empty(nbytes, dtype=torch.uint8, device=f"cuda:{ordinal}")
+    su, sd = torch.cuda.Stream(ordinal), torch.cuda.Stream(ordinal)
+    res = []
+    for _ in range(3):
+        eu = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+        ed = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+        with torch.cuda.stream(su):
+            eu[0].record(); du.copy_(hu, non_blocking=True); eu[1].record()
+        with torch.cuda.stream(sd):
+            ed[0].record(); hd.copy_(dd, non_blocking=True); ed[1].record()
+        torch.cuda.synchronize(ordinal)
+        res.append((nbytes / (eu[0].elapsed_time(eu[1]) * 1e-3) / 1e9, nbytes / (ed[0].elapsed_time(ed[1]) * 1e-3) / 1e9))
+    return max(r[0] for r in res), max(r[1] for r in res)
+
+
 def covered_tokens(bundle, d, key):
     """Tokens of the packed layout covered by plan device d's resident blocks (`key`:
     resident_q / resident_kv / resident_o): the rows a rank's host I/O copies."""
@@ -445,9 +467,17 @@ def measure(args, cfg_name, N, world, rank, rank_mode, barrier, reduce, steps, w
             rows_o = sum(covered_tokens(bundle, d, "resident_o") for d in range(N))
         else:
             rows_q = rows_kv = rows_o = T
+        # PCIe roofline of the e2e step: the same byte counts at the pinned-copy bandwidth of
+        # this box, measured here in both directions at once (the steps overlap them)
+        h2d_b = 2 * rows_q * H * 256 + 2 * rows_kv * G * 256
+        d2h_b = rows_o * H * (256 + 4) + rows_q * H * 256 + 2 * rows_kv * G * 256
+        up_gbs, down_gbs = pcie_gbs(ordinal)
+        pcie_ms = max(h2d_b / (up_gbs * 1e9), d2h_b / (down_gbs * 1e9)) * 1e3
         e2e = {"value": F_total / (e_ms * 1e-3) / 1e12, "unit": "TFLOP/s", "ms_per_step": e_ms,
-               "h2d_bytes_per_step": 2 * rows_q * H * 256 + 2 * rows_kv * G * 256,           # Q, dO; K, V
-               "d2h_bytes_per_step": rows_o * H * (256 + 4) + rows_q * H * 256 + 2 * rows_kv * G * 256,  # O+LSE; dQ; dK, dV
+               "pcie_gbs_measured": {"h2d": up_gbs, "d2h": down_gbs, "how": "1 GiB pinned copies, both directions at once"},
+               "pcie_bound_ms": pcie_ms, "pcie_frac": pcie_ms / e_ms,
+               "h2d_bytes_per_step": h2d_b,   # Q, dO; K, V
+               "d2h_bytes_per_step": d2h_b,   # O + LSE; dQ; dK, dV
                "path": "dcpx_load_inputs_host + dcpx_forward_host + dcpx_backward_host (pinned host buffers; "
                        "asynchronous: uploads/downloads overlap compute across steps"
                        + ("; every rank copies only its plan device's token rows)" if rank_mode else ")")}
