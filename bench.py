@@ -343,12 +343,13 @@ def measure(args, cfg_name, N, world, rank, rank_mode, barrier, reduce, steps, w
         return rf, rb
 
     # kernel timing: CUDA events around every attention launch on its stream (executor option
-    # kernel_timing), read back at the end of each call
-    ex.set_option("kernel_timing", 1)
+    # kernel_timing = 2: accumulated without blocking the host, read after the timed region)
+    ex.set_option("kernel_timing", 2)
     for _ in range(warmup):
         step()
     for d in devs:
         torch.cuda.synchronize(d)
+    ex.kernel_times()  # drop the warm-up launches
     barrier()
     fwd_k, bwd_k, fwd_n, bwd_n, launches = [], [], [], [], 0
     with ClockSampler(list(range(min(N, torch.cuda.device_count()))) if (rank == 0 and sample_clocks) else []) as clk:
@@ -361,8 +362,6 @@ def measure(args, cfg_name, N, world, rank, rank_mode, barrier, reduce, steps, w
         t0 = time.perf_counter()
         for _ in range(steps):
             rf, rb = step()
-            fwd_k.append(rf["attn_ms_sum"]); bwd_k.append(rb["attn_ms_sum"])
-            fwd_n.append(rf["attn_launches"]); bwd_n.append(rb["attn_launches"])
             launches += rf["kernel_launches"] + rb["kernel_launches"] + 3 * len(devs)  # + q/k/v scatters
         for d in devs:
             with torch.cuda.device(d):
@@ -370,6 +369,9 @@ def measure(args, cfg_name, N, world, rank, rank_mode, barrier, reduce, steps, w
                 torch.cuda.synchronize(d)
         wall = time.perf_counter() - t0
         barrier()
+    kt = ex.kernel_times()
+    fwd_k, bwd_k = [kt["fwd_ms_sum"] / steps], [kt["bwd_ms_sum"] / steps]
+    fwd_n, bwd_n = [kt["fwd_launches"] / steps], [kt["bwd_launches"] / steps]
     ex.set_option("kernel_timing", 0)
     total_ms = max(starts[d].elapsed_time(ends[d]) for d in devs)
     ms_step = reduce(total_ms / steps, "max")

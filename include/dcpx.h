@@ -263,11 +263,19 @@ dcpx_status dcpx_set_streams(dcpx_ctx* ctx, int n, void* const* streams);
 dcpx_status dcpx_check_plans(int nplans, const dcpx_plan_view* plans, const dcpx_graph_view* graph,
                              const dcpx_mask_view* masks, char* err, int64_t cap);
 
+/* GPU time of the attention kernel launches (K1 / K1b) recorded since the last read with
+ * option "kernel_timing" = 2 (CUDA events around each launch on its stream, accumulated
+ * without blocking the host): ms[0] / ms[1] = forward / backward summed over this context's
+ * devices, ms[2] / ms[3] = the same, max over devices; launches[0..1] = launch counts.
+ * Synchronises on those events, then resets the accumulation. */
+dcpx_status dcpx_kernel_times(dcpx_ctx* ctx, double* ms, int32_t* launches);
+
 /* Test / introspection hooks (not part of the reference surface). */
 /* Device pointers of the slot arenas of plan device `dev`: kind 0 Q, 1 KV, 2 O, 3 LSE. */
 dcpx_status dcpx_debug_arena(dcpx_ctx* ctx, int dev, int kind, void** ptr, int64_t* slot_rows);
 /* Executor options: "fuse_reductions", "remap_copies", "timing" (report device_ms; blocks
- * the host at the end of each call; default off), "kernel_timing", "trace", "sm_transfers",
+ * the host at the end of each call; default off), "kernel_timing" (1: per-call attention
+ * kernel times in the report, blocking; 2: deferred, see dcpx_kernel_times), "trace", "sm_transfers",
  * "sm_reserve", "bwd_order", "bwd_window", "bwd_window_min_steps", "bwd_merge_heads". */
 dcpx_status dcpx_set_option(dcpx_ctx* ctx, const char* key, int64_t value);
 

@@ -136,6 +136,13 @@ dcpx_status dcpx_check_plans(int nplans, const dcpx_plan_view* plans, const dcpx
   return st;
 }
 
+dcpx_status dcpx_kernel_times(dcpx_ctx* ctx, double* ms, int32_t* launches) {
+  return guarded(ctx, [&](dcpx::Executor& ex) {
+    if (!ms || !launches) throw dcpx::Failure(DCPX_ERROR, "dcpx_kernel_times: null output");
+    ex.kernel_times(ms, launches);
+  });
+}
+
 dcpx_status dcpx_debug_arena(dcpx_ctx* ctx, int dev, int kind, void** ptr, int64_t* slot_rows) {
   return guarded(ctx, [&](dcpx::Executor& ex) { ex.debug_arena(dev, kind, ptr, slot_rows); });
 }
@@ -154,7 +161,7 @@ dcpx_status dcpx_set_option(dcpx_ctx* ctx, const char* key, int64_t value) {
     else if (k == "bwd_window_min_steps") ex.opt.bwd_window_min_steps = static_cast<int>(value);
     else if (k == "bwd_merge_heads") ex.opt.bwd_merge_heads = static_cast<int>(value);
     else if (k == "sm_reserve") ex.opt.sm_reserve = static_cast<int>(value);
-    else if (k == "kernel_timing") ex.opt.kernel_timing = value != 0;
+    else if (k == "kernel_timing") ex.opt.kernel_timing = static_cast<int>(value);
     else throw dcpx::Failure(DCPX_ERROR, "unknown option " + k);
   });
 }

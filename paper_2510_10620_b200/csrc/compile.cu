@@ -232,6 +232,8 @@ void Executor::compile_device(int d) {
     zero(D.d_o, nq * SR * 256);
     zero(D.lse2, nq * SR * 4);
     zero(D.delta, nq * SR * 4);
+    zero(D.dq_acc, nq * SR * 512);     // every backward leaves them zeroed for the next one
+    zero(D.dkv_acc, nkv * 2 * SR * 512);
     D.tm_do = make_tmap(D.d_o, nq * SR, kBwdQRows);
     D.tm_dq = make_tmap_f32(D.dq_acc, nq * SR, kBwdQRows);
     D.tm_q = make_tmap(D.q, std::max<int64_t>(1, D.cap_q) * SR);

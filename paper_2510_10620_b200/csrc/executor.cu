@@ -77,6 +77,9 @@ Executor::Executor(int ndev, const int* ordinals, int transport, int rank)
     CUDA_OK(cudaEventCreate(&dev_[d].t1));
     CUDA_OK(cudaEventCreateWithFlags(&dev_[d].ev_join, cudaEventDisableTiming));
     CUDA_OK(cudaEventCreateWithFlags(&dev_[d].ev_done, cudaEventDisableTiming));
+    CUDA_OK(cudaStreamCreateWithFlags(&dev_[d].as, cudaStreamNonBlocking));
+    CUDA_OK(cudaEventCreateWithFlags(&dev_[d].aux_done, cudaEventDisableTiming));
+    CUDA_OK(cudaEventCreateWithFlags(&dev_[d].bwd_end, cudaEventDisableTiming));
   }
   if (R_ > 0) {
     DeviceGuard g(ordinals_[0]);
@@ -140,6 +143,31 @@ void Executor::await_peer_pulls() {
   }
 }
 
+void Executor::kernel_times(double* ms, int32_t* launches) {
+  for (int k = 0; k < 4; ++k) ms[k] = 0;
+  launches[0] = launches[1] = 0;
+  for (int d = 0; d < R_; ++d) {
+    if (!local(d)) continue;
+    DevState& D = dev_[d];
+    DeviceGuard gd(D.ordinal);
+    double dev_ms[2] = {0, 0};
+    for (size_t k = 0; k < D.next_kev; ++k) {
+      CUDA_OK(cudaEventSynchronize(D.kev[k].second));
+      float t = 0;
+      CUDA_OK(cudaEventElapsedTime(&t, D.kev[k].first, D.kev[k].second));
+      const int pass = D.kev_pass[k];
+      dev_ms[pass] += t;
+      ++launches[pass];
+    }
+    for (int p = 0; p < 2; ++p) {
+      ms[p] += dev_ms[p];
+      ms[2 + p] = std::max(ms[2 + p], dev_ms[p]);
+    }
+    D.next_kev = 0;
+    D.kev_pass.clear();
+  }
+}
+
 void Executor::set_streams(int n, const cudaStream_t* s) {
   if (host_only_) throw Failure(DCPX_ERROR, "host-only context");
   if (n != R_) throw Failure(DCPX_ERROR, "dcpx_set_streams: one stream per plan device");
@@ -197,6 +225,7 @@ Executor::~Executor() {
     DeviceGuard g(d.ordinal);
     if (d.cs) cudaStreamSynchronize(d.cs);
     if (d.ms) cudaStreamSynchronize(d.ms);
+    if (d.as) cudaStreamSynchronize(d.as);
   }
   if (R_ > 0) {
     DeviceGuard g(dev_[0].ordinal);
@@ -220,6 +249,9 @@ Executor::~Executor() {
     for (auto& e : d.tev) { cudaEventDestroy(e.first); cudaEventDestroy(e.second); }
     if (d.ev_join) cudaEventDestroy(d.ev_join);
     if (d.ev_done) cudaEventDestroy(d.ev_done);
+    if (d.aux_done) cudaEventDestroy(d.aux_done);
+    if (d.bwd_end) cudaEventDestroy(d.bwd_end);
+    if (d.as) cudaStreamDestroy(d.as);
     if (d.t0) cudaEventDestroy(d.t0);
     if (d.t1) cudaEventDestroy(d.t1);
     if (d.cs) cudaStreamDestroy(d.cs);
@@ -358,8 +390,10 @@ std::pair<cudaEvent_t, cudaEvent_t> Executor::trace_events(int d) {
   return D.tev[D.next_tev++];
 }
 
-std::pair<cudaEvent_t, cudaEvent_t> Executor::kernel_events(int d) {
+std::pair<cudaEvent_t, cudaEvent_t> Executor::kernel_events(int d, int pass) {
   auto& D = dev_[d];
+  D.kev_pass.resize(D.next_kev + 1);
+  D.kev_pass[D.next_kev] = pass;
   if (D.next_kev == D.kev.size()) {
     DeviceGuard g(D.ordinal);
     cudaEvent_t a, b;

@@ -114,7 +114,12 @@ struct DevState {
   cudaEvent_t t0 = nullptr, t1 = nullptr;
   int launches = 0;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> kev;  // per attention launch (kernel_timing)
+  std::vector<int> kev_pass;                             // 0 forward / 1 backward, per used pair
   size_t next_kev = 0;
+  // the fp32 gradient accumulators are re-zeroed on `as` after each backward (bwd_end), off the
+  // compute stream; the next backward's compute waits for aux_done
+  cudaStream_t as = nullptr;
+  cudaEvent_t aux_done = nullptr, bwd_end = nullptr;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> tev;  // per traced op (trace), a separate pool
   size_t next_tev = 0;
   // stream contract with the caller: every call starts after the work already enqueued on
@@ -134,7 +139,9 @@ struct Options {
   bool remap_copies = true;
   bool check_rows = false;
   bool timing = false;  // per-call device_ms in the report (blocks the host at the end of each call)
-  bool kernel_timing = false;
+  // CUDA events around every attention launch: 1 = read back at the end of each call (in the
+  // report; blocks the host), 2 = accumulated without blocking, read by kernel_times()
+  int kernel_timing = 0;
   bool trace = false;
   bool sm_transfers = true;   // LOCAL transfers by copy kernel (false: DMA copy engines)
   int sm_reserve = -1;        // SMs left free of attention CTAs for transfer kernels (-1: auto)
@@ -196,6 +203,9 @@ class Executor {
   void backward(const void* const* d_o, void* const* dq, void* const* dk, void* const* dv, dcpx_report* rep,
                 bool host);
   void synchronize();
+  // kernel_timing 2: GPU time of the attention launches since the last read, per pass:
+  // ms[0..1] summed over local devices (fwd, bwd), ms[2..3] max over devices; resets
+  void kernel_times(double* ms, int32_t* launches);
   // the caller's stream on each plan device (nullptr entry: the legacy default stream)
   void set_streams(int n, const cudaStream_t* s);
   void debug_arena(int dev, int kind, void** ptr, int64_t* rows);
@@ -223,7 +233,7 @@ class Executor {
   void fill_report(dcpx_report* rep, bool bwd);
   void simulate_order();
   cudaEvent_t event(int d);
-  std::pair<cudaEvent_t, cudaEvent_t> kernel_events(int d);
+  std::pair<cudaEvent_t, cudaEvent_t> kernel_events(int d, int pass);
   std::pair<cudaEvent_t, cudaEvent_t> trace_events(int d);
   void join_caller();     // cs of every local device waits for the caller's stream
   void release_caller();  // the caller's stream waits for cs of every local device

@@ -111,7 +111,10 @@ void Executor::forward(void* const* o_out, float* const* lse_out, dcpx_report* r
   for (int d = 0; d < R_; ++d) {
     DevState& D = dev_[d];
     D.next_event = 0;
-    D.next_kev = 0;
+    if (opt.kernel_timing != 2) {  // (deferred timing accumulates until kernel_times())
+      D.next_kev = 0;
+      D.kev_pass.clear();
+    }
     D.next_tev = 0;
     D.launches = 0;
     if (!local(d)) continue;
@@ -150,7 +153,7 @@ void Executor::forward(void* const* o_out, float* const* lse_out, dcpx_report* r
         p.sched = D.sched_ctr;
         p.sched_base = D.sched_base;
         D.sched_base += static_cast<uint32_t>(op.num_units + grid);
-        if (opt.kernel_timing) { ke = kernel_events(d); CUDA_OK(cudaEventRecord(ke.first, D.cs)); }
+        if (opt.kernel_timing) { ke = kernel_events(d, 0); CUDA_OK(cudaEventRecord(ke.first, D.cs)); }
         launch_attn_fwd(D.tm_q, D.tm_kv, p, grid, D.cs);
         if (opt.kernel_timing) CUDA_OK(cudaEventRecord(ke.second, D.cs));
         ++D.launches;
@@ -312,7 +315,7 @@ void Executor::fill_report(dcpx_report* rep, bool bwd) {
       if (op.kind == OpKind::kFwdAttn) rep->units += bwd ? op.bnum_units : op.num_units;
     if (bwd) rep->windowed += dev_[d].bwd_windowed;
   }
-  if (opt.kernel_timing) {
+  if (opt.kernel_timing == 1) {
     double mx = 0;
     for (int d = 0; d < R_; ++d) {
       if (!local(d)) continue;
@@ -367,7 +370,10 @@ void Executor::backward(const void* const* d_o, void* const* dq, void* const* dk
   for (int d = 0; d < R_; ++d) {
     DevState& D = dev_[d];
     D.next_event = 0;
-    D.next_kev = 0;
+    if (opt.kernel_timing != 2) {  // (deferred timing accumulates until kernel_times())
+      D.next_kev = 0;
+      D.kev_pass.clear();
+    }
     D.next_tev = 0;
     D.launches = 0;
     if (!local(d)) continue;
@@ -406,9 +412,9 @@ void Executor::backward(const void* const* d_o, void* const* dq, void* const* dk
     if (!local(d)) continue;
     DevState& D = dev_[d];
     DeviceGuard gd(D.ordinal);
-    const int64_t SR = D.slot_rows;
-    CUDA_OK(cudaMemsetAsync(D.dq_acc, 0, std::max<int64_t>(1, D.cap_q) * SR * 512, D.cs));
-    CUDA_OK(cudaMemsetAsync(D.dkv_acc, 0, std::max<int64_t>(1, D.cap_kv) * 2 * SR * 512, D.cs));
+    // the fp32 accumulators were zeroed on the aux stream right after the previous backward
+    // (overlapping the next forward; zero at prepare for the first call)
+    CUDA_OK(cudaStreamWaitEvent(D.cs, D.aux_done, 0));
     launch_row_copy(D.scatter_do.dj, D.cs, reinterpret_cast<int64_t>(ddo[d]), 0);
     launch_delta(D.prep.dj, D.o, D.lse, D.d_o, D.delta, D.lse2, D.cs);
     D.launches += 2;
@@ -467,7 +473,7 @@ void Executor::backward(const void* const* d_o, void* const* dq, void* const* dk
           p.sched = D.sched_ctr;
           p.sched_base = D.sched_base;
           D.sched_base += static_cast<uint32_t>(op.bnum_units + grid);
-          if (opt.kernel_timing) { ke = kernel_events(d); CUDA_OK(cudaEventRecord(ke.first, D.cs)); }
+          if (opt.kernel_timing) { ke = kernel_events(d, 1); CUDA_OK(cudaEventRecord(ke.first, D.cs)); }
           launch_attn_bwd(D.tm_q64, D.tm_do, D.tm_kv, D.tm_dq, D.tm_dkv, p, grid, D.cs);
           if (opt.kernel_timing) CUDA_OK(cudaEventRecord(ke.second, D.cs));
           ++D.launches;
@@ -568,6 +574,20 @@ void Executor::backward(const void* const* d_o, void* const* dq, void* const* dk
     if (fr.empty()) fr.push_back(staging_event(0));
     CUDA_OK(cudaEventRecord(fr[0], d2h_));
   }
+  for (int d = 0; d < R_; ++d) {
+    // re-zero the fp32 accumulators for the next backward on the aux stream, once this
+    // call's gathers (and gradient returns) have read them: off the critical path, it
+    // overlaps whatever the caller runs next (the next step's input load and forward)
+    if (!local(d)) continue;
+    DevState& D = dev_[d];
+    DeviceGuard gd(D.ordinal);
+    const int64_t SR = D.slot_rows;
+    CUDA_OK(cudaEventRecord(D.bwd_end, D.cs));
+    CUDA_OK(cudaStreamWaitEvent(D.as, D.bwd_end, 0));
+    CUDA_OK(cudaMemsetAsync(D.dq_acc, 0, std::max<int64_t>(1, D.cap_q) * SR * 512, D.as));
+    CUDA_OK(cudaMemsetAsync(D.dkv_acc, 0, std::max<int64_t>(1, D.cap_kv) * 2 * SR * 512, D.as));
+    CUDA_OK(cudaEventRecord(D.aux_done, D.as));
+  }
   release_caller();  // dq / dk / dv (device buffers) are ready in the caller's stream order
   fill_report(rep, true);
 }
@@ -578,6 +598,7 @@ void Executor::synchronize() {
     DeviceGuard gd(D.ordinal);
     CUDA_OK(cudaStreamSynchronize(D.cs));
     CUDA_OK(cudaStreamSynchronize(D.ms));
+    CUDA_OK(cudaStreamSynchronize(D.as));
   }
   if (R_ > 0) {
     DeviceGuard gd(dev_[0].ordinal);

@@ -31,7 +31,7 @@ STATUS = {0: "OK", 1: "Error", 2: "DeadlockError", 3: "TagMismatchError", 4: "Bu
 EXPORTS = ["dcpx_create", "dcpx_create_rank", "dcpx_rank_export", "dcpx_rank_connect", "dcpx_prepare",
            "dcpx_load_inputs", "dcpx_load_inputs_host", "dcpx_forward", "dcpx_forward_host",
            "dcpx_backward", "dcpx_backward_host", "dcpx_load_inputs_dev", "dcpx_forward_dev",
-           "dcpx_backward_dev", "dcpx_synchronize", "dcpx_set_streams", "dcpx_check_plans",
+           "dcpx_backward_dev", "dcpx_synchronize", "dcpx_set_streams", "dcpx_check_plans", "dcpx_kernel_times",
            "dcpx_debug_arena", "dcpx_set_option", "dcpx_trace", "dcpx_last_error", "dcpx_version",
            "dcpx_destroy"]
 
@@ -59,9 +59,10 @@ def lib():
                      "dcpx_forward_host", "dcpx_backward", "dcpx_backward_host",
                      "dcpx_load_inputs_dev", "dcpx_forward_dev", "dcpx_backward_dev",
                      "dcpx_synchronize", "dcpx_debug_arena", "dcpx_set_option", "dcpx_set_streams",
-                     "dcpx_check_plans"):
+                     "dcpx_check_plans", "dcpx_kernel_times"):
             getattr(L, name).restype = C.c_int
         L.dcpx_set_streams.argtypes = [C.c_void_p, C.c_int, C.c_void_p]
+        L.dcpx_kernel_times.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
         L.dcpx_check_plans.argtypes = [C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_char_p, C.c_int64]
         L.dcpx_create.argtypes = [C.c_int, C.POINTER(C.c_int), C.c_int, C.POINTER(C.c_void_p)]
         L.dcpx_create_rank.argtypes = [C.c_int, C.c_int, C.c_int, C.POINTER(C.c_void_p)]
@@ -231,6 +232,15 @@ class DCPExecutor:
 
     def synchronize(self):
         self._check(lib().dcpx_synchronize(self._h))
+
+    def kernel_times(self) -> dict:
+        """Attention-kernel GPU time since the last read (option kernel_timing = 2):
+        fwd/bwd ms summed over this context's devices and max over devices, launch counts."""
+        ms = (C.c_double * 4)()
+        n = (C.c_int32 * 2)()
+        self._check(lib().dcpx_kernel_times(self._h, ms, n))
+        return dict(fwd_ms_sum=ms[0], bwd_ms_sum=ms[1], fwd_ms_max=ms[2], bwd_ms_max=ms[3],
+                    fwd_launches=n[0], bwd_launches=n[1])
 
     def trace(self):
         """Op spans of the last call when option "trace" is set: list of dicts."""
