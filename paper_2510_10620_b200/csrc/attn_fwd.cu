@@ -60,6 +60,9 @@ constexpr int kSoftExpPairs = DCPX_SOFT_EXP_PAIRS;
 #define DCPX_FWD_SPLIT_P 0
 #endif
 constexpr bool kSplitP = DCPX_FWD_SPLIT_P != 0;
+// Also measured and not kept (round 2): row max and row sum as 4 / 8 independent chains
+// instead of one FMNMX3 / FADD chain: cfg3 8.00 -> 8.22 / 8.19 ms (the other tile's warp
+// hides the chain latency; the extra live registers cost more).
 // Also measured and not kept: the MMA warp issuing the two tiles' PV + next S in the order
 // their P becomes ready (polling both barriers) instead of tile 0 first: 8.0 -> 9.0 ms (cfg3).
 

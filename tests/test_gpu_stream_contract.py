@@ -71,3 +71,37 @@ def test_inputs_and_outputs_ordered_by_caller_stream(side_stream):
             assert np.array_equal(a, b), name
         else:
             assert np.abs(a - b).max() <= 4e-3 * max(1.0, np.abs(b).max()), name
+
+
+def test_deferred_kernel_timing():
+    """Option kernel_timing = 2: the attention launches of several calls are timed without
+    blocking the host and read back once by dcpx_kernel_times (then reset); option 1 puts
+    the same per-call numbers in the report."""
+    import torch
+    bundle = bundle_for(MIXED_SPECS, H=4, G=2, block=256, R=2)
+    (q, k, v), _ = inputs(bundle, seed=63)
+    T, H, G = bundle.total_tokens, bundle.H, bundle.G
+    with DCPExecutor([0] * bundle.R) as ex:
+        ex.prepare(bundle)
+        o = torch.zeros((T, H, 128), dtype=torch.bfloat16, device="cuda")
+        lse = torch.zeros((H, T), device="cuda")
+        dq = torch.zeros_like(o)
+        dk = torch.zeros((T, G, 128), dtype=torch.bfloat16, device="cuda")
+        dv = torch.zeros_like(dk)
+        d_o = torch.randn((T, H, 128), device="cuda").to(torch.bfloat16)
+        ex.set_option("kernel_timing", 1)
+        ex.load_inputs(q.cuda(), k.cuda(), v.cuda())
+        rf = ex.forward(o, lse)
+        rb = ex.backward(d_o, dq, dk, dv)
+        assert rf["attn_launches"] > 0 and rb["attn_launches"] > 0 and rf["attn_ms_sum"] > 0
+        ex.set_option("kernel_timing", 2)
+        for _ in range(3):
+            ex.load_inputs(q.cuda(), k.cuda(), v.cuda())
+            r2 = ex.forward(o, lse)
+            ex.backward(d_o, dq, dk, dv)
+        assert r2["attn_launches"] == 0  # deferred: nothing in the per-call report
+        kt = ex.kernel_times()
+        assert kt["fwd_launches"] == 3 * rf["attn_launches"] and kt["bwd_launches"] == 3 * rb["attn_launches"]
+        assert kt["fwd_ms_sum"] > 0 and kt["bwd_ms_sum"] > 0 and kt["bwd_ms_max"] <= kt["bwd_ms_sum"]
+        again = ex.kernel_times()
+        assert again["fwd_launches"] == 0 and again["bwd_ms_sum"] == 0
