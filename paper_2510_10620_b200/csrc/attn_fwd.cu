@@ -410,10 +410,17 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       }
       FWD_T(te0);
       // ---- epilogue: O / l, LSE, optional merge with the destination's current value.
-      // (Prefetching the merge operands to L2 at the start of the unit measured neutral and
-      // cost register spills, so they are read here.)
+      // The merge operands (this row's previous O, 256 B, and LSE) are loaded before the wait
+      // for the unit's last PV, all 16 vectors at once, so their global-memory latency
+      // overlaps it instead of costing four round trips after it.
       float lse_prev = -CUDART_INF_F;
-      if (merge && row_valid) lse_prev = p.lse_arena[orow];
+      uint4 prev[16];
+      if (merge && row_valid) {
+        const uint4* src = reinterpret_cast<const uint4*>(out);
+#pragma unroll
+        for (int k = 0; k < 16; ++k) prev[k] = src[k];
+        lse_prev = p.lse_arena[orow];
+      }
       const float lse_new = l > 0.f ? (m_used + __log2f(l)) * 0.69314718055994531f : -CUDART_INF_F;
       const float inv_l = l > 0.f ? 1.f / l : 0.f;
       float w_new = 1.f, w_prev = 0.f, lse_out = lse_new;
@@ -433,37 +440,28 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         ++cnt_o;
         tc_fence_after();
       }
-#pragma unroll 1
-      for (int c = 0; c < 128; c += 32) {
-        float o[32];
-        {
-          uint32_t oraw[32];
-          if (has) {
-            tmem_ld32(lane_addr + o_col + c, oraw);
-            tmem_wait_ld();
-          } else {
+      const float scale_new = inv_l * w_new;
 #pragma unroll
-            for (int k = 0; k < 32; ++k) oraw[k] = 0u;
-          }
+      for (int c = 0; c < 4; ++c) {
+        uint32_t oraw[32];
+        if (has) {
+          tmem_ld32(lane_addr + o_col + 32 * c, oraw);
+          tmem_wait_ld();
+        } else {
 #pragma unroll
-          for (int k = 0; k < 32; ++k) o[k] = __uint_as_float(oraw[k]);
+          for (int k = 0; k < 32; ++k) oraw[k] = 0u;
         }
         if (row_valid) {
-          uint4* dst = reinterpret_cast<uint4*>(out + c);
-          uint4 prev[4];
-          if (merge) {
-#pragma unroll
-            for (int k = 0; k < 4; ++k) prev[k] = dst[k];
-          }
+          uint4* dst = reinterpret_cast<uint4*>(out + 32 * c);
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
             uint32_t w[4];
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
-              float a = o[k * 8 + 2 * e] * inv_l * w_new;
-              float b = o[k * 8 + 2 * e + 1] * inv_l * w_new;
+              float a = __uint_as_float(oraw[k * 8 + 2 * e]) * scale_new;
+              float b = __uint_as_float(oraw[k * 8 + 2 * e + 1]) * scale_new;
               if (merge) {
-                const uint32_t pv = (&prev[k].x)[e];
+                const uint32_t pv = (&prev[4 * c + k].x)[e];
                 const __nv_bfloat162 pb = *reinterpret_cast<const __nv_bfloat162*>(&pv);
                 a = fmaf(__bfloat162float(pb.x), w_prev, a);
                 b = fmaf(__bfloat162float(pb.y), w_prev, b);
