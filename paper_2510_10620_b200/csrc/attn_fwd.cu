@@ -194,10 +194,11 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         const FwdUnit U = p.units[u];
         const FwdStep* steps = p.steps + U.step_begin;
         bool has[2] = {false, false};
+        int last[2] = {-1, -1};  // each tile's last step: its O is final after that PV
         for (int j = 0; j < U.step_count; ++j) {
           const uint32_t c = steps[j].cls;
-          has[0] |= cls_of(c, 0) != 0;
-          has[1] |= cls_of(c, 1) != 0;
+          if (cls_of(c, 0)) { has[0] = true; last[0] = j; }
+          if (cls_of(c, 1)) { has[1] = true; last[1] = j; }
         }
         int issued[2] = {-1, -1};
         bool first[2] = {true, true};
@@ -247,6 +248,12 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
               }
               __syncwarp();
             }
+            // O_t is final once this tile's last PV retires: signal its epilogue now rather
+            // than after the other tile's last PV (which waits for that tile's softmax)
+            if (j == last[t]) {
+              if (elect_one()) umma_commit(&bars.o_full[t]);
+              __syncwarp();
+            }
             ++cnt_p[t];
             first[t] = false;
             if (j + 1 < U.step_count && cls_of(steps[j + 1].cls, t)) {
@@ -263,8 +270,6 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         if (elect_one()) {
           // a unit without steps (rows that attend nothing) still took a Q buffer
           if (U.step_count == 0) umma_commit(&bars.q_empty);
-          for (int t = 0; t < 2; ++t)
-            if (has[t]) umma_commit(&bars.o_full[t]);
         }
         __syncwarp();
 #pragma unroll
