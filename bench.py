@@ -24,6 +24,9 @@ from __future__ import annotations
 import argparse
 import json
 import os
+
+# before torch creates a CUDA context (see paper_2510_10620_b200/__init__.py)
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
 import platform
 import subprocess
 import sys
@@ -344,7 +347,7 @@ def measure(args, cfg_name, N, world, rank, rank_mode, barrier, reduce, steps, w
 
     # kernel timing: CUDA events around every attention launch on its stream (executor option
     # kernel_timing = 2: accumulated without blocking the host, read after the timed region)
-    ex.set_option("kernel_timing", 2)
+    ex.set_option("kernel_timing", args.kernel_timing)
     for _ in range(warmup):
         step()
     for d in devs:
@@ -362,6 +365,9 @@ def measure(args, cfg_name, N, world, rank, rank_mode, barrier, reduce, steps, w
         t0 = time.perf_counter()
         for _ in range(steps):
             rf, rb = step()
+            if args.kernel_timing == 1:
+                fwd_k.append(rf["attn_ms_sum"]); bwd_k.append(rb["attn_ms_sum"])
+                fwd_n.append(rf["attn_launches"]); bwd_n.append(rb["attn_launches"])
             launches += rf["kernel_launches"] + rb["kernel_launches"] + 3 * len(devs)  # + q/k/v scatters
         for d in devs:
             with torch.cuda.device(d):
@@ -369,9 +375,10 @@ def measure(args, cfg_name, N, world, rank, rank_mode, barrier, reduce, steps, w
                 torch.cuda.synchronize(d)
         wall = time.perf_counter() - t0
         barrier()
-    kt = ex.kernel_times()
-    fwd_k, bwd_k = [kt["fwd_ms_sum"] / steps], [kt["bwd_ms_sum"] / steps]
-    fwd_n, bwd_n = [kt["fwd_launches"] / steps], [kt["bwd_launches"] / steps]
+    if args.kernel_timing == 2:
+        kt = ex.kernel_times()
+        fwd_k, bwd_k = [kt["fwd_ms_sum"] / steps], [kt["bwd_ms_sum"] / steps]
+        fwd_n, bwd_n = [kt["fwd_launches"] / steps], [kt["bwd_launches"] / steps]
     ex.set_option("kernel_timing", 0)
     total_ms = max(starts[d].elapsed_time(ends[d]) for d in devs)
     ms_step = reduce(total_ms / steps, "max")
@@ -518,6 +525,9 @@ def main():
                     help="SMs kept free of attention CTAs for transfer kernels (-1: executor default)")
     ap.add_argument("--placement", default="dcp", choices=["dcp", "ring", "zigzag"],
                     help="plan placement: DCP (default) or the paper's baselines (cfg2 only)")
+    ap.add_argument("--kernel-timing", type=int, default=2, choices=[1, 2],
+                    help="attention-launch events: 2 = read after the timed region (default), "
+                         "1 = read at the end of every call (blocks the host each step)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--mode", default="rank", choices=["rank", "single"],

@@ -1,0 +1,10 @@
+"""B200-native executor for DCP execution plans."""
+import os
+
+# The executor overlaps its compute stream with a comm stream whose kernels the compute
+# kernels may wait on. CUDA multiplexes a process's streams onto CUDA_DEVICE_MAX_CONNECTIONS
+# hardware work queues (default 8); two streams sharing a queue run in submission order, which
+# serialises transfers behind compute (measured: cfg2 on 4 B200s 2300 vs 2530 TFLOP/s). The
+# variable is read when the CUDA context is created, so this takes effect when the package is
+# imported before the process's first CUDA call; callers that set it themselves win.
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")

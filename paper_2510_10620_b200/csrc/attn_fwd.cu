@@ -141,6 +141,11 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         if (u < 0) break;
         const FwdUnit U = p.units[u];
         const int ntiles = U.n_rows > kTileRows ? 2 : 1;
+        const int division = (U.flags >> 8) & 0xff;
+        if (p.rdy && division > 0) {  // persistent launch: the fetches of divisions <= this landed
+          if (elect_one()) wait_counter(p.rdy, p.rdy_target[division]);
+          __syncwarp();
+        }
         mbar_wait(&bars.q_empty, (it & 1) ^ 1);
         if (elect_one()) {
           mbar_arrive_expect_tx(&bars.q_full, ntiles * 32768);
@@ -420,6 +425,10 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       // overlaps it instead of costing four round trips after it.
       float lse_prev = -CUDART_INF_F;
       uint4 prev[16];
+      if (merge && U.dep >= 0) {  // persistent launch: the earlier division's unit has stored
+        if (lane == 0) wait_stamp(p.unit_done + 2 * U.dep + t, p.epoch);
+        __syncwarp();
+      }
       if (merge && row_valid) {
         const uint4* src = reinterpret_cast<const uint4*>(out);
 #pragma unroll
@@ -481,6 +490,14 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       if (has) {
         tc_fence_before();
         mbar_arrive(&bars.o_empty[t]);
+      }
+      if (p.unit_done) {  // persistent launch: publish this tile's output (all 128 rows stored)
+        named_bar_sync(1 + t, 128);
+        if (r == 0) {
+          __threadfence();
+          st_release_gpu(p.unit_done + 2 * u + t, p.epoch);
+          red_release_gpu_add(p.done + ((U.flags >> 8) & 0xff), 1u);
+        }
       }
       FWD_T(te1);
       FWD_ACC(6, te0, te1);

@@ -160,6 +160,8 @@ dcpx_status dcpx_set_option(dcpx_ctx* ctx, const char* key, int64_t value) {
     else if (k == "bwd_window") ex.opt.bwd_window = static_cast<int>(value);
     else if (k == "bwd_window_min_steps") ex.opt.bwd_window_min_steps = static_cast<int>(value);
     else if (k == "bwd_merge_heads") ex.opt.bwd_merge_heads = static_cast<int>(value);
+    else if (k == "persistent") ex.opt.persistent = static_cast<int>(value);
+    else if (k == "aux_zero") ex.opt.aux_zero = static_cast<int>(value);
     else if (k == "sm_reserve") ex.opt.sm_reserve = static_cast<int>(value);
     else if (k == "kernel_timing") ex.opt.kernel_timing = static_cast<int>(value);
     else throw dcpx::Failure(DCPX_ERROR, "unknown option " + k);

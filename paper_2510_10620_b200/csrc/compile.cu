@@ -8,6 +8,8 @@
 #include <algorithm>
 #include <array>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <tuple>
@@ -324,6 +326,7 @@ void Executor::compile_device(int d) {
         std::vector<FwdUnit> units;
         std::vector<FwdStep> steps;
         std::vector<int64_t> unit_cost;
+        std::vector<int> unit_oblock;  // output block of each unit (persistent-launch checks)
         for (const auto& grp : groups_of[i]) {
           const auto& i0 = P.items[grp.items[0]];
           const int n_q = static_cast<int>(i0.q_end - i0.q_begin);
@@ -334,8 +337,9 @@ void Executor::compile_device(int d) {
             U.q_row0 = static_cast<int32_t>(i0.q_slot * SR + 256 * pr);
             U.n_rows = std::min(256, n_q - 256 * pr);
             U.out_row0 = static_cast<int32_t>(D.o_phys[grp.target] * SR + 256 * pr);
-            U.flags = grp.merge_prev ? 1 : 0;
+            U.flags = (grp.merge_prev ? 1 : 0) | (std::min(I.division, 255) << 8);
             U.q_local0 = 256 * pr;
+            U.dep = -1;
             U.step_begin = static_cast<int32_t>(steps.size());
             int64_t cost = 0;
             for (int idx : grp.items) {
@@ -357,6 +361,7 @@ void Executor::compile_device(int d) {
             U.step_count = static_cast<int32_t>(steps.size()) - U.step_begin;
             units.push_back(U);
             unit_cost.push_back(cost * 1000 + U.n_rows);
+            unit_oblock.push_back(g_.comp_blocks[P.items[grp.items[0]].comp_id].o_block);
           }
         }
         // longest-processing-time-first order (the kernels take units in list order from a
@@ -370,6 +375,10 @@ void Executor::compile_device(int d) {
         op.steps = upload(d, steps);
         op.items = upload(d, masks);
         op.num_units = static_cast<int>(sorted.size());
+        op.h_units = sorted;
+        op.h_steps = steps;
+        op.h_items = masks;
+        for (size_t k : order) op.h_unit_oblock.push_back(unit_oblock[k]);
         op.grid = std::min(op.num_units, num_sms(D.ordinal));
         // -- backward units: one per (kv slot, 128-row kv sub-tile, window of bwd_window
         //    q tiles of one item). Windowing bounds the rows a wave of CTAs touches: with
@@ -582,6 +591,115 @@ void Executor::compile_device(int d) {
     const int src = remap_dst2src[r.slot];
     D.final_o_slot.push_back(D.o_phys[src >= 0 ? src : r.slot]);
   }
+}
+
+// Persistent cross-division forward for plan device d (multi-device plans): all attention
+// instructions' units concatenated in division order into one launch. The kernel then needs
+// device-side ordering instead of launch boundaries: units of division t wait for the
+// transfers of division t (rdy), a unit merging into an earlier division's output waits for
+// that unit's epilogue (dep / unit_done), and a receive waits for the units of the divisions
+// whose attention precedes its launch in program order (done), i.e. those that read the
+// slots it overwrites. Eligible when nothing but transfers
+// sit between the attention instructions (no unfused merge or copy) and every physical O slot
+// keeps one output block for the whole forward.
+void Executor::build_persistent_fwd(int d) {
+  DevState& D = dev_[d];
+  D.pfwd = false;
+  D.pf_first = -1;
+  if (!opt.persistent || R_ < 2 || transport_ != DCPX_TRANSPORT_LOCAL) return;
+  // The launch spins on transfers that run on the SMs it leaves free; plan devices sharing a
+  // GPU would fill those SMs with each other's persistent CTAs (one process) or only run
+  // between time slices (ranks in separate processes), so a single-GPU emulation of a
+  // multi-device plan keeps one launch per division.
+  if (rank_ < 0) {
+    for (int e = 0; e < R_; ++e)
+      if (e != d && dev_[e].ordinal == D.ordinal) return;
+  } else {
+    int n = 0;
+    CUDA_OK(cudaGetDeviceCount(&n));
+    if (n < R_) return;
+  }
+  const int T = plans_[d].divisions;
+  if (T + 1 > 255) return;
+  std::vector<int> attn;
+  for (size_t i = 0; i < D.prog.size(); ++i)
+    if (D.prog[i].kind == OpKind::kFwdAttn && D.prog[i].num_units > 0) attn.push_back(static_cast<int>(i));
+  if (attn.size() < 2) return;
+  for (int i = attn.front(); i <= attn.back(); ++i) {
+    const Op& op = D.prog[i];
+    if (op.kind == OpKind::kMerge || op.kind == OpKind::kCopy) return;
+    if (op.kind == OpKind::kCommLaunch && op.send && !op.resident_only) return;
+    if (op.kind == OpKind::kFwdAttn && op.division >= T) return;
+  }
+  std::vector<FwdUnit> units;
+  std::vector<FwdStep> steps;
+  std::vector<ItemMask> items;
+  std::map<int32_t, int> last_writer;  // out_row0 -> unit
+  std::map<int64_t, int> slot_block;   // physical O slot -> output block
+  std::vector<uint32_t> done_target(static_cast<size_t>(T) + 1, 0);
+  for (int i : attn) {
+    const Op& op = D.prog[i];
+    const int32_t s0 = static_cast<int32_t>(steps.size()), m0 = static_cast<int32_t>(items.size());
+    for (size_t k = 0; k < op.h_units.size(); ++k) {
+      FwdUnit U = op.h_units[k];
+      U.step_begin += s0;
+      const int slot = static_cast<int>(U.out_row0 / D.slot_rows);
+      auto [sb, fresh] = slot_block.try_emplace(slot, op.h_unit_oblock[k]);
+      if (!fresh && sb->second != op.h_unit_oblock[k]) return;  // O slot reused by another output
+      auto lw = last_writer.find(U.out_row0);
+      if (U.flags & 1) {
+        if (lw == last_writer.end()) return;  // merges with a value no unit of this launch wrote
+        if (units[static_cast<size_t>(lw->second)].n_rows != U.n_rows) return;  // per-tile stamps
+        U.dep = lw->second;
+      } else if (lw != last_writer.end()) {
+        return;  // overwrites an earlier unit's output unordered
+      }
+      last_writer[U.out_row0] = static_cast<int>(units.size());
+      done_target[static_cast<size_t>(op.division)] += U.n_rows > kTileRows ? 2 : 1;
+      units.push_back(U);
+    }
+    for (FwdStep S : op.h_steps) {
+      S.item += m0;
+      steps.push_back(S);
+    }
+    items.insert(items.end(), op.h_items.begin(), op.h_items.end());
+  }
+  // the comm stream runs the transfers in program order (division ascending) and each adds 1
+  // to one counter, so "every fetch of divisions <= t landed" is a cumulative count (a
+  // division may read blocks fetched for an earlier one and have no transfers of its own)
+  std::vector<uint32_t> rdy_target(static_cast<size_t>(T) + 1, 0);
+  for (const Op& op : D.prog)
+    if (op.kind == OpKind::kCommWait && op.division < T) ++rdy_target[static_cast<size_t>(op.division)];
+  // slot reuse: without the persistent launch a receive starts after every attention op that
+  // precedes its launch in program order; here it waits for those ops' divisions on the device
+  std::map<std::string, int> wait_divs;
+  int divs_before = 0;
+  for (const Op& op : D.prog) {
+    if (op.kind == OpKind::kFwdAttn && op.num_units > 0) divs_before = std::max(divs_before, op.division + 1);
+    if (op.kind == OpKind::kCommLaunch && !op.send) wait_divs[op.tag] = divs_before;
+  }
+  for (Op& op : D.prog)
+    if (op.kind == OpKind::kCommWait && op.division < T) {
+      const auto w = wait_divs.find(op.tag);
+      if (w == wait_divs.end() || w->second > op.division) return;  // (would wait on its own readers)
+      op.pf_wait_divs = w->second;
+    }
+  for (int t = 1; t <= T; ++t) rdy_target[static_cast<size_t>(t)] += rdy_target[static_cast<size_t>(t) - 1];
+  D.pf_units = upload(d, units);
+  D.pf_steps = upload(d, steps);
+  D.pf_items = upload(d, items);
+  D.pf_num_units = static_cast<int>(units.size());
+  D.pf_grid = std::min(D.pf_num_units, num_sms(D.ordinal));
+  D.prdy_target = upload(d, rdy_target);
+  D.pdone_target = upload(d, done_target);
+  D.pctr = static_cast<uint32_t*>(alloc(d, sizeof(uint32_t) * 2 * (static_cast<size_t>(T) + 1)));
+  D.punit_done = static_cast<uint32_t*>(alloc(d, sizeof(uint32_t) * 2 * units.size()));
+  if (local(d)) {
+    DeviceGuard g(D.ordinal);
+    CUDA_OK(cudaMemset(D.punit_done, 0, sizeof(uint32_t) * 2 * units.size()));
+  }
+  D.pf_first = attn.front();
+  D.pfwd = true;
 }
 
 void Executor::build_io_jobs(int d) {

@@ -65,10 +65,15 @@ Executor::Executor(int ndev, const int* ordinals, int transport, int rank)
                         cudaHostAllocMapped | cudaHostAllocPortable));
   std::memset(diag_, 0, sizeof(uint32_t) * (1 + 4 * 64));
   for (int d = 0; d < R_; ++d) {
-    DeviceGuard g(ordinals_[d]);
     dev_[d].ordinal = ordinals_[d];
+    // streams and events only for the devices this process drives (per-rank mode: one); every
+    // extra stream on a GPU raises the odds that the compute and comm streams share one of
+    // its hardware work queues (CUDA_DEVICE_MAX_CONNECTIONS), which serialises them
+    if (!local(d)) continue;
+    DeviceGuard g(ordinals_[d]);
     set_watchdog_buffer_fwd(diag_);
     set_watchdog_buffer_bwd(diag_);
+    preload_movers();
     CUDA_OK(cudaStreamCreateWithFlags(&dev_[d].cs, cudaStreamNonBlocking));
     int lo = 0, hi = 0;
     CUDA_OK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
@@ -604,6 +609,7 @@ void Executor::prepare(int nplans, const dcpx_plan_view* plans, const dcpx_graph
   for (int d = 0; d < R_; ++d) {
     dev_[d].slot_rows = slot_rows;
     compile_device(d);
+    build_persistent_fwd(d);
   }
   // ---- transfer jobs (owned by the receiver) and input / output jobs
   build_transfer_jobs();
@@ -640,6 +646,7 @@ void Executor::prepare(int nplans, const dcpx_plan_view* plans, const dcpx_graph
     epoch_ = pulls_epoch_ = 0;
     connected_ = false;
   }
+  acc_dirty_ = false;  // the accumulators were zeroed when allocated (compile_device)
   prepared_ = true;
 }
 

@@ -66,6 +66,12 @@ struct Op {
   ItemMask* items = nullptr;
   int num_units = 0, grid = 0;
   uint64_t flops = 0;
+  // host copies of the forward lists (a persistent launch concatenates them) and the output
+  // block each unit writes
+  std::vector<FwdUnit> h_units;
+  std::vector<FwdStep> h_steps;
+  std::vector<ItemMask> h_items;
+  std::vector<int> h_unit_oblock;
   // kMerge / kCopy
   JobList jobs;
   int32_t* src_rows = nullptr;
@@ -82,6 +88,9 @@ struct Op {
   // comm
   int send = 0, peer = 0;
   bool resident_only = false;  // a send of resident Q / KV slots only
+  // persistent forward, receive side: the transfer overwrites slots once the units of
+  // divisions < pf_wait_divs are done (the attention ops before its launch in program order)
+  int pf_wait_divs = 0;
   std::string tag;
   std::vector<dcpx_block_slot> blocks;
   uint64_t bytes = 0;
@@ -126,6 +135,19 @@ struct DevState {
   // `caller` (its inputs) and `caller` waits for the call's device work (its outputs)
   cudaStream_t caller = cudaStreamLegacy;
   cudaEvent_t ev_join = nullptr, ev_done = nullptr;
+  // persistent cross-division forward: one launch for all divisions' units,
+  // gated device-side (FwdParams::rdy / done / unit_done); pf_first = the op that launches
+  // it (the device's first attention), the other attention ops launch nothing
+  bool pfwd = false;
+  int pf_first = -1;
+  FwdUnit* pf_units = nullptr;
+  FwdStep* pf_steps = nullptr;
+  ItemMask* pf_items = nullptr;
+  int pf_num_units = 0, pf_grid = 0;
+  uint32_t* pctr = nullptr;          // rdy[T + 1] then done[T + 1]
+  uint32_t* prdy_target = nullptr;   // [T + 1] transfers per division
+  uint32_t* pdone_target = nullptr;  // [T + 1] (unit, tile) epilogues per division
+  uint32_t* punit_done = nullptr;    // [2 * pf_num_units] epoch stamps
   // dynamic unit scheduler of the attention kernels: a device counter that every launch
   // advances by num_units + grid, and its host-side running value (sched_produce)
   uint32_t* sched_ctr = nullptr;
@@ -156,6 +178,11 @@ struct Options {
   int bwd_window_min_steps = 128;
   // windows span every item of one q block (the heads of the GQA group) instead of one item
   int bwd_merge_heads = 1;
+  // multi-device plans: run each device's forward divisions as one persistent launch
+  int persistent = 0;
+  // re-zero the fp32 gradient accumulators on the aux stream after each backward (1) or on the
+  // compute stream at the start of the next one (0)
+  int aux_zero = 1;
 };
 
 class Executor;
@@ -228,6 +255,9 @@ class Executor {
   void trace_collect();
   void compile_device(int d);
   void compile_attention(int d, int ins_index, std::vector<bool>& fused_red);
+  void build_persistent_fwd(int d);
+  void zero_accumulators(int d, cudaStream_t s);  // the fp32 dQ / dK,dV accumulators
+  bool acc_dirty_ = false;  // the last backward did not re-zero them (aux_zero = 0)
   void build_io_jobs(int d);
   void build_bwd_jobs();
   void fill_report(dcpx_report* rep, bool bwd);

@@ -10,6 +10,8 @@
 #include <cuda_bf16.h>
 #include <math_constants.h>
 
+#include <cstdio>
+
 #include "movers.h"
 
 namespace dcpx {
@@ -255,7 +257,59 @@ __global__ void flag_wait_kernel(FlagList fl, int n, uint32_t epoch) {
   __syncthreads();
 }
 
+// ------------------------------------------------- persistent-launch counters (comm stream)
+// Adds 1 to a device counter with release semantics, after the stream's previous work (the
+// transfer whose data the counter publishes).
+__global__ void counter_add_kernel(uint32_t* c) {
+  __threadfence();
+  asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(c) : "memory");
+}
+
+// Waits until c[i] >= target[i] for every i < n (the comm stream's receive may overwrite
+// slots only once the attention units of the divisions that read them have finished).
+__global__ void counter_wait_kernel(const uint32_t* c, const uint32_t* target, int n) {
+  const int i = threadIdx.x;
+  if (i < n) {
+    const long long t0 = clock64();
+    for (;;) {
+      uint32_t v;
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(c + i) : "memory");
+      if (v >= target[i]) break;
+      __nanosleep(128);
+#ifdef DCPX_WATCHDOG_REPORT
+      if (clock64() - t0 > 8000000000LL) {
+        printf("[counter_wait] done[%d] = %u < %u\n", i, v, target[i]);
+        __trap();
+      }
+#endif
+      if (clock64() - t0 > 40000000000LL) __trap();  // ~20 s: a unit never finished
+    }
+  }
+  __syncthreads();
+}
+
 // ---------------------------------------------------------------------------- launchers
+// Loads every kernel of this file on the current device. With lazy module loading (the CUDA
+// 12 default) the first launch of a kernel loads it, which waits for the device to go idle:
+// a transfer or counter kernel first launched while a persistent attention kernel spins on
+// its completion would never start.
+void preload_movers() {
+  cudaFuncAttributes a;
+  cudaFuncGetAttributes(&a, row_copy_kernel);
+  cudaFuncGetAttributes(&a, merge_kernel);
+  cudaFuncGetAttributes(&a, delta_kernel);
+  cudaFuncGetAttributes(&a, return_accum_kernel);
+  cudaFuncGetAttributes(&a, accum_bf16_kernel);
+  cudaFuncGetAttributes(&a, f32_to_bf16_kernel);
+  cudaFuncGetAttributes(&a, flag_set_kernel);
+  cudaFuncGetAttributes(&a, flag_wait_kernel);
+  cudaFuncGetAttributes(&a, counter_add_kernel);
+  cudaFuncGetAttributes(&a, counter_wait_kernel);
+}
+void launch_counter_add(uint32_t* c, cudaStream_t s) { counter_add_kernel<<<1, 1, 0, s>>>(c); }
+void launch_counter_wait(const uint32_t* c, const uint32_t* target, int n, cudaStream_t s) {
+  if (n > 0) counter_wait_kernel<<<1, 32 * ((n + 31) / 32), 0, s>>>(c, target, n);
+}
 void launch_flag_set(uint32_t* flag, uint32_t epoch, cudaStream_t s) { flag_set_kernel<<<1, 1, 0, s>>>(flag, epoch); }
 void launch_flag_wait(const uint32_t* const* flags, int n, uint32_t epoch, cudaStream_t s) {
   if (n <= 0) return;

@@ -38,6 +38,9 @@ struct DevJobs {
 };
 
 void launch_row_copy(const DevJobs& j, cudaStream_t s, int64_t src_adjust = 0, int64_t dst_adjust = 0);
+void preload_movers();  // per current device, before any launch that others spin on
+void launch_counter_add(uint32_t* c, cudaStream_t s);
+void launch_counter_wait(const uint32_t* c, const uint32_t* target, int n, cudaStream_t s);
 void launch_merge(const DevJobs& j, const int32_t* src_rows, __nv_bfloat16* o, float* lse, cudaStream_t s);
 void launch_delta(const DevJobs& j, const __nv_bfloat16* o, const float* lse, const __nv_bfloat16* d_o,
                   float* delta, float* lse2, cudaStream_t s);

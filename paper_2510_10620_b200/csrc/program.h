@@ -39,9 +39,11 @@ struct FwdUnit {
   int32_t step_begin;  // first FwdStep
   int32_t step_count;
   int32_t out_row0;    // O/LSE arena row of q tile 0 (destination slot)
-  int32_t flags;       // bit0: merge with the destination's current (O, LSE)
+  int32_t flags;       // bit0: merge with the destination's current (O, LSE);
+                       // bits 8-15: division (persistent cross-division launch)
   int32_t q_local0;    // q row index (within the item) of q tile 0
-  int32_t _pad;
+  int32_t dep;         // persistent launch: the unit of an earlier division whose output this
+                       // unit merges with (its epilogue waits for that unit's), else -1
 };
 
 struct FwdStep {
@@ -114,6 +116,17 @@ struct FwdParams {
   float scale_log2;  // log2(e) / sqrt(D)
   uint32_t sched_base;  // dynamic-scheduler counter value at this launch
   uint32_t* sched;      // the device's scheduler counter (see sched_produce)
+  // Persistent cross-division launch (all divisions' units in one launch; null otherwise):
+  // a unit of division t > 0 starts loading once *rdy >= rdy_target[t] (every fetch of the
+  // divisions <= t landed: each transfer adds 1 on the comm stream); each (unit, tile) epilogue
+  // publishes unit_done[2 u + tile] = epoch and adds 1 to done[division] (the comm stream
+  // waits on done before a receive overwrites slots freed by earlier divisions).
+  uint32_t* rdy;
+  const uint32_t* rdy_target;
+  uint32_t* done;
+  uint32_t* unit_done;
+  uint32_t epoch;
+  int32_t _pad;
 };
 
 }  // namespace dcpx

@@ -123,11 +123,14 @@ void Executor::forward(void* const* o_out, float* const* lse_out, dcpx_report* r
   }
   await_peer_pulls();
   ++epoch_;
+  const int T = R_ ? plans_[0].divisions : 0;
   std::map<std::string, cudaEvent_t> send_ev, recv_ev;
   std::vector<cudaEvent_t> ready_ev(static_cast<size_t>(R_));
   for (int d = 0; d < R_; ++d) {  // resident Q / KV were scattered on cs before this call
     if (!local(d)) continue;
     DeviceGuard gd(dev_[d].ordinal);
+    if (dev_[d].pfwd)  // persistent launch: this call's dependency counters start at zero
+      CUDA_OK(cudaMemsetAsync(dev_[d].pctr, 0, sizeof(uint32_t) * 2 * (static_cast<size_t>(T) + 1), dev_[d].cs));
     ready_ev[d] = event(d);
     CUDA_OK(cudaEventRecord(ready_ev[d], dev_[d].cs));
   }
@@ -143,16 +146,29 @@ void Executor::forward(void* const* o_out, float* const* lse_out, dcpx_report* r
     switch (op.kind) {
       case OpKind::kFwdAttn: {
         if (!op.num_units) break;
+        const bool pers = D.pfwd;
+        if (pers && static_cast<int>(i) != D.pf_first) break;  // part of the persistent launch
         FwdParams p{};
-        p.units = op.units; p.steps = op.steps; p.items = op.items; p.ranges = D.ranges;
-        p.o_arena = D.o; p.lse_arena = D.lse; p.num_units = op.num_units;
+        p.units = pers ? D.pf_units : op.units;
+        p.steps = pers ? D.pf_steps : op.steps;
+        p.items = pers ? D.pf_items : op.items;
+        p.ranges = D.ranges;
+        p.o_arena = D.o; p.lse_arena = D.lse;
+        p.num_units = pers ? D.pf_num_units : op.num_units;
         p.slot_rows = static_cast<int32_t>(D.slot_rows);
         p.scale_log2 = static_cast<float>(1.4426950408889634 / std::sqrt(static_cast<double>(g_.D)));
+        if (pers) {
+          p.rdy = D.pctr;
+          p.rdy_target = D.prdy_target;
+          p.done = D.pctr + T + 1;
+          p.unit_done = D.punit_done;
+          p.epoch = epoch_;
+        }
         std::pair<cudaEvent_t, cudaEvent_t> ke{};
-        const int grid = attn_grid(d, op.grid);
+        const int grid = attn_grid(d, pers ? D.pf_grid : op.grid);
         p.sched = D.sched_ctr;
         p.sched_base = D.sched_base;
-        D.sched_base += static_cast<uint32_t>(op.num_units + grid);
+        D.sched_base += static_cast<uint32_t>(p.num_units + grid);
         if (opt.kernel_timing) { ke = kernel_events(d, 0); CUDA_OK(cudaEventRecord(ke.first, D.cs)); }
         launch_attn_fwd(D.tm_q, D.tm_kv, p, grid, D.cs);
         if (opt.kernel_timing) CUDA_OK(cudaEventRecord(ke.second, D.cs));
@@ -170,6 +186,10 @@ void Executor::forward(void* const* o_out, float* const* lse_out, dcpx_report* r
       case OpKind::kCommLaunch: {
         if (op.send && op.resident_only) {
           send_ev[op.tag] = ready_ev[d];  // resident inputs: ready since load / preprocess
+        } else if (!op.send && D.pfwd && op.division < T) {
+          // persistent launch: the slots are free once the units of divisions <= division - 2
+          // are done, which the transfer waits for on the device (kCommWait below)
+          recv_ev[op.tag] = ready_ev[d];
         } else {
           cudaEvent_t e = event(d);
           CUDA_OK(cudaEventRecord(e, D.cs));
@@ -179,6 +199,7 @@ void Executor::forward(void* const* o_out, float* const* lse_out, dcpx_report* r
         break;
       }
       case OpKind::kCommWait: {
+        const bool pers_xfer = D.pfwd && op.division < T;
         if (transport_ == DCPX_TRANSPORT_NCCL) {
           nccl_transfer(op.peer, d, op.xfer, send_ev.at(op.tag), recv_ev.at(op.tag));
           cursor.to(D.ordinal);
@@ -188,6 +209,8 @@ void Executor::forward(void* const* o_out, float* const* lse_out, dcpx_report* r
           else
             CUDA_OK(cudaStreamWaitEvent(D.ms, send_ev.at(op.tag), 0));
           CUDA_OK(cudaStreamWaitEvent(D.ms, recv_ev.at(op.tag), 0));
+          if (pers_xfer)  // the units that read the slots' previous blocks are done
+            launch_counter_wait(D.pctr + T + 1, D.pdone_target, op.pf_wait_divs, D.ms);
           ts.split(kTraceXfer);
           if (opt.sm_transfers) {
             launch_row_copy(op.jobs.dj, D.ms);
@@ -195,6 +218,7 @@ void Executor::forward(void* const* o_out, float* const* lse_out, dcpx_report* r
           } else {
             copy_engine(op.xfer, D.ms);
           }
+          if (pers_xfer) launch_counter_add(D.pctr, D.ms);  // one more fetch landed (cumulative)
         }
         cudaEvent_t e = event(d);
         CUDA_OK(cudaEventRecord(e, D.ms));
@@ -331,6 +355,8 @@ void Executor::fill_report(dcpx_report* rep, bool bwd) {
       rep->attn_launches += static_cast<int32_t>(D.next_kev);
       rep->attn_ms_sum += sum;
       mx = std::max(mx, sum);
+      D.next_kev = 0;  // read: a later switch to deferred timing starts from an empty pool
+      D.kev_pass.clear();
     }
     rep->attn_ms = mx;
   }
@@ -415,6 +441,7 @@ void Executor::backward(const void* const* d_o, void* const* dq, void* const* dk
     // the fp32 accumulators were zeroed on the aux stream right after the previous backward
     // (overlapping the next forward; zero at prepare for the first call)
     CUDA_OK(cudaStreamWaitEvent(D.cs, D.aux_done, 0));
+    if (acc_dirty_) zero_accumulators(d, D.cs);  // (the previous backward left them)
     launch_row_copy(D.scatter_do.dj, D.cs, reinterpret_cast<int64_t>(ddo[d]), 0);
     launch_delta(D.prep.dj, D.o, D.lse, D.d_o, D.delta, D.lse2, D.cs);
     D.launches += 2;
@@ -581,15 +608,22 @@ void Executor::backward(const void* const* d_o, void* const* dq, void* const* dk
     if (!local(d)) continue;
     DevState& D = dev_[d];
     DeviceGuard gd(D.ordinal);
-    const int64_t SR = D.slot_rows;
+    if (!opt.aux_zero) continue;  // zeroed at the start of the next backward instead
     CUDA_OK(cudaEventRecord(D.bwd_end, D.cs));
     CUDA_OK(cudaStreamWaitEvent(D.as, D.bwd_end, 0));
-    CUDA_OK(cudaMemsetAsync(D.dq_acc, 0, std::max<int64_t>(1, D.cap_q) * SR * 512, D.as));
-    CUDA_OK(cudaMemsetAsync(D.dkv_acc, 0, std::max<int64_t>(1, D.cap_kv) * 2 * SR * 512, D.as));
+    zero_accumulators(d, D.as);
     CUDA_OK(cudaEventRecord(D.aux_done, D.as));
   }
+  acc_dirty_ = !opt.aux_zero;
   release_caller();  // dq / dk / dv (device buffers) are ready in the caller's stream order
   fill_report(rep, true);
+}
+
+void Executor::zero_accumulators(int d, cudaStream_t s) {
+  DevState& D = dev_[d];
+  const int64_t SR = D.slot_rows;
+  CUDA_OK(cudaMemsetAsync(D.dq_acc, 0, std::max<int64_t>(1, D.cap_q) * SR * 512, s));
+  CUDA_OK(cudaMemsetAsync(D.dkv_acc, 0, std::max<int64_t>(1, D.cap_kv) * 2 * SR * 512, s));
 }
 
 void Executor::synchronize() {

@@ -172,6 +172,47 @@ __device__ __forceinline__ uint32_t ld_acquire_cta(const uint32_t* p) {
   return v;
 }
 
+// ---- device-side dependency counters (persistent cross-division launches) ------------------
+__device__ __forceinline__ uint32_t ld_acquire_gpu(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_gpu(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void red_release_gpu_add(uint32_t* p, uint32_t v) {
+  asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+// Spins until *p reaches `target` (global, acquire); traps after ~20 s so a missing signal
+// surfaces as a launch error. Then orders the generic-proxy acquire before later async-proxy
+// (TMA) reads of the data the signal published.
+__device__ __forceinline__ void wait_counter(const uint32_t* p, uint32_t target) {
+  if (ld_acquire_gpu(p) < target) {
+    const uint64_t t0 = global_ns();
+    while (ld_acquire_gpu(p) < target) {
+      __nanosleep(64);  // (exponential back-off to 2 us measured: no difference)
+#ifdef DCPX_WATCHDOG_REPORT
+      if (global_ns() - t0 > 5000000000ull) {  // report before the mbarrier watchdog fires
+        printf("[wait_counter] block %d: counter %u < target %u\n", blockIdx.x, ld_acquire_gpu(p), target);
+        __trap();
+      }
+#endif
+      if (global_ns() - t0 > 20000000000ull) __trap();
+    }
+  }
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+// Spins until *p == v (an epoch stamp), acquire.
+__device__ __forceinline__ void wait_stamp(const uint32_t* p, uint32_t v) {
+  if (ld_acquire_gpu(p) == v) return;
+  const uint64_t t0 = global_ns();
+  while (ld_acquire_gpu(p) != v) {
+    __nanosleep(64);
+    if (global_ns() - t0 > 20000000000ull) __trap();
+  }
+}
+
 // ---- dynamic unit scheduler -------------------------------------------------------------
 // Persistent kernels take their work units from a global counter instead of a static
 // blockIdx-strided walk: one lane of a scheduler warp fetches unit indices (atomicAdd) into
@@ -182,7 +223,10 @@ __device__ __forceinline__ uint32_t ld_acquire_cta(const uint32_t* p) {
 // The counter is never reset: every launch advances it by exactly num_units + gridDim.x
 // (each CTA's scheduler stops after its first fetch past the end), so the host passes the
 // launch's base value and keeps the running sum (modulo 2^32).
-constexpr int kSchedRing = 8;
+#ifndef DCPX_SCHED_RING
+#define DCPX_SCHED_RING 2
+#endif
+constexpr int kSchedRing = DCPX_SCHED_RING;
 struct SchedRing {
   uint64_t full[kSchedRing], empty[kSchedRing];
   int32_t unit[kSchedRing];

@@ -23,6 +23,9 @@ def main():
     v = torch.randn((T, G, 128), device="cuda").to(torch.bfloat16)
     ex = DCPExecutor([d % ng for d in range(b.R)])
     ex.set_option("timing", 1)
+    for kv in filter(None, os.environ.get("PROBE_OPTS", "").split(",")):  # e.g. persistent=0
+        key, val = kv.split("=")
+        ex.set_option(key, int(val))
     ex.prepare(b)
     o = torch.empty_like(q)
     lse = torch.empty((H, T), device="cuda")
@@ -48,7 +51,7 @@ def main():
     rb = ex.backward(q, dq, dk, dv)
     tb = ex.trace()
     print(f"{name} on {ng} GPUs: fwd {rf['device_ms']:.3f} ms, bwd {rb['device_ms']:.3f} ms")
-    for label, tr in (("fwd", tf), ("bwd", tb)):
+    for label, tr in (("fwd", tf), ("bwd", tb))[: 1 if os.environ.get("PROBE_FWD_ONLY") else 2]:
         for d in range(b.R):
             rows = [t for t in tr if t["dev"] == d]
             s = "  ".join(f"{t['kind']}{t['division']}[{t['start']:.2f}-{t['end']:.2f}]" if t['kind'] != 'launch'
