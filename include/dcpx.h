@@ -276,7 +276,13 @@ dcpx_status dcpx_debug_arena(dcpx_ctx* ctx, int dev, int kind, void** ptr, int64
 /* Executor options: "fuse_reductions", "remap_copies", "timing" (report device_ms; blocks
  * the host at the end of each call; default off), "kernel_timing" (1: per-call attention
  * kernel times in the report, blocking; 2: deferred, see dcpx_kernel_times), "trace", "sm_transfers",
- * "sm_reserve", "bwd_order", "bwd_window", "bwd_window_min_steps", "bwd_merge_heads". */
+ * "sm_reserve", "bwd_order", "bwd_window", "bwd_window_min_steps", "bwd_merge_heads",
+ * "persistent" (1: one forward launch per device for all divisions, ordered on the device;
+ * default 0), "aux_zero" (1, default: the gradient accumulators are re-zeroed on an aux
+ * stream after each backward; 0: at the start of the next one).
+ * The executor overlaps a compute and a comm stream per device; set
+ * CUDA_DEVICE_MAX_CONNECTIONS=32 (or more) before the process creates its CUDA context so
+ * they do not share a hardware work queue (the Python package does this on import). */
 dcpx_status dcpx_set_option(dcpx_ctx* ctx, const char* key, int64_t value);
 
 /* Op trace of the last forward/backward (option "trace"): rows of 7 doubles
