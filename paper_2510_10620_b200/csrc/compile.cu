@@ -689,7 +689,9 @@ void Executor::build_persistent_fwd(int d) {
   D.pf_steps = upload(d, steps);
   D.pf_items = upload(d, items);
   D.pf_num_units = static_cast<int>(units.size());
-  D.pf_grid = std::min(D.pf_num_units, num_sms(D.ordinal));
+  // at least two SMs stay free whatever sm_reserve says: the comm stream's counter / flag
+  // kernels the launch spins on need somewhere to run
+  D.pf_grid = std::min(D.pf_num_units, num_sms(D.ordinal) - 2);
   D.prdy_target = upload(d, rdy_target);
   D.pdone_target = upload(d, done_target);
   D.pctr = static_cast<uint32_t*>(alloc(d, sizeof(uint32_t) * 2 * (static_cast<size_t>(T) + 1)));

@@ -309,17 +309,37 @@ int Executor::attn_grid(int d, int grid) const {
   return std::min(grid, cap);
 }
 
-// LOCAL transport on the DMA copy engines: one peer copy per contiguous block component,
-// issued on the receiver's comm stream so NVLink traffic never competes with the
-// persistent attention kernels for SMs.
+// LOCAL transport on the DMA copy engines (option sm_transfers = 0), issued on the receiver's
+// comm stream so NVLink traffic never competes with the attention kernels for SMs. A block
+// component is one contiguous run of slot rows on both sides; runs that continue each other
+// on both sides are merged into one cudaMemcpyAsync (one call per 256 KiB component keeps
+// the host issuing thousands of copies per step).
 void Executor::copy_engine(const std::vector<RowCopyJob>& jobs, cudaStream_t s) {
+  char *dst = nullptr, *src = nullptr;
+  size_t run = 0;
+  auto flush = [&] {
+    if (run) CUDA_OK(cudaMemcpyAsync(dst, src, run, cudaMemcpyDefault, s));
+    run = 0;
+  };
   for (const auto& j : jobs) {
     if (j.src_stride == j.row_bytes && j.dst_stride == j.row_bytes) {
-      CUDA_OK(cudaMemcpyAsync(j.dst, j.src, static_cast<size_t>(j.rows) * j.row_bytes, cudaMemcpyDefault, s));
+      const size_t n = static_cast<size_t>(j.rows) * j.row_bytes;
+      char* d = static_cast<char*>(j.dst);
+      char* c = const_cast<char*>(static_cast<const char*>(j.src));
+      if (run && dst + run == d && src + run == c) {
+        run += n;
+      } else {
+        flush();
+        dst = d;
+        src = c;
+        run = n;
+      }
     } else {
+      flush();
       CUDA_OK(cudaMemcpy2DAsync(j.dst, j.dst_stride, j.src, j.src_stride, j.row_bytes, j.rows, cudaMemcpyDefault, s));
     }
   }
+  flush();
 }
 
 // ---- op tracing (option "trace"): device-time spans of every executed op ------------------

@@ -13,11 +13,13 @@ from common import MIXED_SPECS, bundle_for, inputs
 pytestmark = pytest.mark.gpu
 
 
-def _run(bundle, persistent, q, k, v, d_o, ngpu, iters=2):
+def _run(bundle, persistent, q, k, v, d_o, ngpu, iters=2, opts=None):
     import torch
     T, H, G = bundle.total_tokens, bundle.H, bundle.G
     with DCPExecutor([d % ngpu for d in range(bundle.R)]) as ex:
         ex.set_option("persistent", persistent)
+        for key, val in (opts or {}).items():
+            ex.set_option(key, val)
         ex.prepare(bundle)
         o = torch.zeros((T, H, 128), dtype=torch.bfloat16, device="cuda")
         lse = torch.zeros((H, T), device="cuda")
