@@ -18,6 +18,7 @@ def main():
     ap.add_argument("--iters", type=int, default=3)
     ap.add_argument("--placement", default="dcp")
     ap.add_argument("--host", action="store_true")
+    ap.add_argument("--opt", action="append", default=[], help="executor option key=value")
     args = ap.parse_args()
     import numpy as np
     import torch
@@ -38,6 +39,9 @@ def main():
     dev = f"cuda:{ordinal}"
     q, k, v, d_o = (x.to(dev) for x in (q, k, v, d_o))
     ex = DCPExecutor(rank=rank, world=world, cuda_ordinal=ordinal)
+    for kv in args.opt:
+        key, val = kv.split("=")
+        ex.set_option(key, int(val))
     ex.prepare(bundle)
     outs = []
     for it in range(args.iters):

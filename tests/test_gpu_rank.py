@@ -52,13 +52,16 @@ def _single_process(R, placement):
                     dk=dk.float().cpu().numpy(), dv=dv.float().cpu().numpy()), rep, bundle
 
 
-@pytest.mark.parametrize("R,placement,host", [(2, "dcp", False), (4, "dcp", True), (4, "zigzag", False),
-                                                (8, "dcp", False)])
-def test_rank_mode_matches_single_process(R, placement, host, tmp_path):
+# the last case runs the persistent cross-division forward in every rank (engaged when each
+# rank has its own GPU; per-division launches otherwise) against the default single process
+@pytest.mark.parametrize("R,placement,host,opts", [(2, "dcp", False, ()), (4, "dcp", True, ()),
+                                                   (4, "zigzag", False, ()), (8, "dcp", False, ()),
+                                                   (4, "zigzag", False, ("persistent=1",))])
+def test_rank_mode_matches_single_process(R, placement, host, opts, tmp_path):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={R}",
            "--master-addr=127.0.0.1", f"--master-port={_free_port()}",
            os.path.join(HERE, "rank_worker.py"), "--out", str(tmp_path), "--iters", "3",
-           "--placement", placement] + (["--host"] if host else [])
+           "--placement", placement] + (["--host"] if host else []) + [f"--opt={o}" for o in opts]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=420)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     want, rep, bundle = _single_process(R, placement)
