@@ -187,8 +187,8 @@ void Executor::forward(void* const* o_out, float* const* lse_out, dcpx_report* r
         if (op.send && op.resident_only) {
           send_ev[op.tag] = ready_ev[d];  // resident inputs: ready since load / preprocess
         } else if (!op.send && D.pfwd && op.division < T) {
-          // persistent launch: the slots are free once the units of divisions <= division - 2
-          // are done, which the transfer waits for on the device (kCommWait below)
+          // persistent launch: the slots are free once the units of the divisions before this
+          // launch point are done, which the transfer waits for on the device (kCommWait)
           recv_ev[op.tag] = ready_ev[d];
         } else {
           cudaEvent_t e = event(d);
