@@ -444,7 +444,7 @@ void Executor::prepare(int nplans, const dcpx_plan_view* plans, const dcpx_graph
   }
   if (!host_only_) free_all();
   for (Staging* st : {&in_st_, &bwd_st_, &fwd_st_})
-    for (int k = 0; k < 2; ++k) {  // (events stay alive in staging_events_ and are reused)
+    for (int k = 0; k < kStagingSlots; ++k) {  // (events stay alive in staging_events_ and are reused)
       st->buf[k] = nullptr;
     }
   fwd_done_ = false;

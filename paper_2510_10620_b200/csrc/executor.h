@@ -17,6 +17,10 @@
 #include "movers.h"
 #include "program.h"
 
+#ifndef DCPX_STAGING_SLOTS
+#define DCPX_STAGING_SLOTS 2
+#endif
+
 namespace dcpx {
 
 // Exception carrying a dcpx_status (mirrors the reference hierarchy, types.hpp:17-45).
@@ -306,14 +310,20 @@ class Executor {
   std::vector<int> alloc_dev_;
   uint32_t* diag_ = nullptr;   // host-mapped watchdog report buffer (see sm100.cuh)
   // Host I/O goes through device-0 staging. load_inputs_host / backward_host are
-  // asynchronous: two staging slots alternate, uploads run on h2d_ and downloads on d2h_
+  // asynchronous: staging slots rotate, uploads run on h2d_ and downloads on d2h_
   // (PCIe is full duplex), so step i+1's uploads and step i's downloads overlap step i's
   // compute; free[k] holds the events after which slot k may be overwritten.
+  static constexpr int kStagingSlots = DCPX_STAGING_SLOTS;
   struct Staging {
-    char* buf[2] = {nullptr, nullptr};
-    std::vector<cudaEvent_t> free[2];  // per plan device (backward: entry 0 only)
-    cudaEvent_t up[2] = {nullptr, nullptr};  // upload into slot k finished (h2d_)
+    char* buf[kStagingSlots] = {};
+    std::vector<cudaEvent_t> free[kStagingSlots];  // per plan device (backward: entry 0 only)
+    cudaEvent_t up[kStagingSlots] = {};             // upload into slot k finished (h2d_)
     int next = 0;
+    int take() {  // the next slot, round robin
+      const int k = next;
+      next = (next + 1) % kStagingSlots;
+      return k;
+    }
   };
   Staging in_st_, bwd_st_, fwd_st_;  // fwd_st_: forward_host outputs (O + LSE), downloaded on d2h_
   cudaStream_t h2d_ = nullptr, d2h_ = nullptr;  // on device 0

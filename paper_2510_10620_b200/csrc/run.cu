@@ -56,8 +56,7 @@ void Executor::load_inputs(const void* const* q, const void* const* k, const voi
     DevState& D0 = dev_[0];
     DeviceGuard gd(D0.ordinal);
     const size_t bq = TT * g_.H * 256, bk = TT * g_.G * 256;
-    slot = in_st_.next;
-    in_st_.next ^= 1;
+    slot = in_st_.take();
     char*& buf = in_st_.buf[slot];
     if (!buf) buf = static_cast<char*>(alloc(0, bq + 2 * bk));
     for (cudaEvent_t e : in_st_.free[slot]) CUDA_OK(cudaStreamWaitEvent(h2d_, e, 0));
@@ -242,8 +241,7 @@ void Executor::forward(void* const* o_out, float* const* lse_out, dcpx_report* r
     // asynchronous like the other host calls: gather into device-0 staging slot k (once
     // the slot's previous download is done), download on d2h_; host buffers are valid after
     // dcpx_synchronize, so the download overlaps the next call's work
-    slot = fwd_st_.next;
-    fwd_st_.next ^= 1;
+    slot = fwd_st_.take();
     char*& buf = fwd_st_.buf[slot];
     if (!buf) buf = static_cast<char*>(alloc(0, TT * g_.H * 256 + TT * g_.H * 4));
     for (int d = 0; d < R_; ++d) {
@@ -412,8 +410,7 @@ void Executor::backward(const void* const* d_o, void* const* dq, void* const* dk
     // dQ/dK/dV come back through the same slot on d2h_ at the end. Asynchronous.
     DevState& D0 = dev_[0];
     DeviceGuard gd(D0.ordinal);
-    slot = bwd_st_.next;
-    bwd_st_.next ^= 1;
+    slot = bwd_st_.take();
     char*& buf = bwd_st_.buf[slot];
     if (!buf) buf = static_cast<char*>(alloc(0, 2 * bq + 2 * bk));
     for (cudaEvent_t e : bwd_st_.free[slot]) CUDA_OK(cudaStreamWaitEvent(h2d_, e, 0));
