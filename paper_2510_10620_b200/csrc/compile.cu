@@ -866,13 +866,12 @@ void Executor::build_bwd_jobs() {
       }
     }
     for (auto& [i, jobs] : ret) D.prog[i].ret = make_jobs(d, jobs);
-    // 3. io: dO scatter to the resident Q slots, Delta/LSE preprocess, gradient gathers
+    // 3. io: Delta/LSE preprocess with the dO scatter to the resident Q slots, gradient gathers
     std::map<std::tuple<int, int, int>, int> qslot_of;  // (seq, head, tile) -> resident Q slot
     for (const auto& r : P.res_q) {
       const auto& db = g_.data_blocks[r.block];
       qslot_of[{db.seq, db.head, db.tile}] = r.slot;
     }
-    std::vector<RowCopyJob> sdo;
     std::vector<RowJob> prep, gq, gk, gv;
     std::vector<int> prep_rows, gq_rows, gk_rows;
     for (size_t k = 0; k < P.res_o.size(); ++k) {
@@ -881,9 +880,7 @@ void Executor::build_bwd_jobs() {
       if (it == qslot_of.end()) throw Failure(DCPX_ERROR, "output block without a co-located Q block (blocks.hpp:42-51)");
       const int64_t tok = g_.seq_offsets[db.seq] + db.tok_begin;
       const int rows = static_cast<int>(db.tok_end - db.tok_begin);
-      sdo.push_back({reinterpret_cast<const char*>((tok * H + db.head) * 256), reinterpret_cast<char*>(D.d_o + it->second * SR * 128),
-                     H * 256, 256, rows, 256});
-      prep.push_back({D.final_o_slot[k] * SR, it->second * SR, 0, rows, 0});
+      prep.push_back({D.final_o_slot[k] * SR, it->second * SR, (tok * H + db.head) * 128, rows, 0});
       prep_rows.push_back(rows);
     }
     for (const auto& r : P.res_q) {
@@ -901,7 +898,6 @@ void Executor::build_bwd_jobs() {
       gv.push_back({(2 * r.slot + 1) * SR, (tok * G + db.head) * 128, G * 128, rows, 0});
       gk_rows.push_back(rows);
     }
-    D.scatter_do = make_jobs(d, sdo);
     D.prep = make_row_jobs(d, prep, prep_rows, 16);
     D.gather_dq = make_row_jobs(d, gq, gq_rows, 16);
     D.gather_dk = make_row_jobs(d, gk, gk_rows, 16);

@@ -120,7 +120,7 @@ struct DevState {
   float *lse2 = nullptr, *delta = nullptr, *dq_acc = nullptr, *dkv_acc = nullptr;
   CUtensorMap tm_do{}, tm_dq{}, tm_q64{};  // backward: 64-row boxes over dO, dQ acc, Q
   CUtensorMap tm_dkv{};                    // backward: dK / dV accumulator, 128-row boxes
-  JobList scatter_do, prep, gather_dq, gather_dk, gather_dv;
+  JobList prep, gather_dq, gather_dk, gather_dv;  // prep: Delta / LSE2 + dO scatter
   std::vector<int32_t> final_o_slot;  // per resident_o entry: physical slot holding the result
   std::vector<cudaEvent_t> events;
   size_t next_event = 0;

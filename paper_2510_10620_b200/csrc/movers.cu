@@ -131,12 +131,15 @@ __global__ void merge_kernel(const MergeJob* __restrict__ jobs, const int32_t* _
   if (sub == 0) lse_arena[(int64_t)J.dst_row0 + row_in_job] = lse_out;
 }
 
-// Backward preprocess for one resident output block: Delta[row] = sum_d dO[row][d] * O[row][d]
-// and LSE in log2 units, written at the block's Q-arena rows. One 16-lane group per row.
+// Backward preprocess for one resident output block, fused with the dO scatter: each row of
+// dO is read once from the caller's packed [T][H][D] buffer (d_o_src + job.b_stride, rows
+// src_stride elements apart), stored into its Q-arena slot row for the backward kernel and
+// the fetches, and dotted with O: Delta[row] = sum_d dO[row][d] * O[row][d], plus LSE in log2
+// units, written at the block's Q-arena rows. One 16-lane group per row.
 __global__ void delta_kernel(const RowJob* __restrict__ jobs, const int32_t* __restrict__ job_of_block,
                              const int32_t* __restrict__ first_chunk, const __nv_bfloat16* o_arena,
-                             const float* lse_arena, const __nv_bfloat16* do_arena, float* delta,
-                             float* lse2) {
+                             const float* lse_arena, const __nv_bfloat16* d_o_src, int64_t src_stride,
+                             __nv_bfloat16* do_arena, float* delta, float* lse2) {
   const int b = blockIdx.x;
   const int j = job_of_block[b];
   const RowJob J = jobs[j];
@@ -145,7 +148,8 @@ __global__ void delta_kernel(const RowJob* __restrict__ jobs, const int32_t* __r
   float s = 0.f;
   if (r < J.rows) {
     const uint4 a = *(reinterpret_cast<const uint4*>(o_arena + ((int64_t)J.a_row0 + r) * 128) + sub);
-    const uint4 d = *(reinterpret_cast<const uint4*>(do_arena + ((int64_t)J.b_row0 + r) * 128) + sub);
+    const uint4 d = __ldcs(reinterpret_cast<const uint4*>(d_o_src + J.b_stride + (int64_t)r * src_stride) + sub);
+    *(reinterpret_cast<uint4*>(do_arena + ((int64_t)J.b_row0 + r) * 128) + sub) = d;
     const __nv_bfloat162* ha = reinterpret_cast<const __nv_bfloat162*>(&a);
     const __nv_bfloat162* hd = reinterpret_cast<const __nv_bfloat162*>(&d);
 #pragma unroll
@@ -325,11 +329,11 @@ void launch_row_copy(const DevJobs& j, cudaStream_t s, int64_t src_adjust, int64
 void launch_merge(const DevJobs& j, const int32_t* src_rows, __nv_bfloat16* o, float* lse, cudaStream_t s) {
   if (j.n_blocks) merge_kernel<<<j.n_blocks, 256, 0, s>>>(static_cast<const MergeJob*>(j.jobs), src_rows, j.job_of_block, j.first_chunk, o, lse);
 }
-void launch_delta(const DevJobs& j, const __nv_bfloat16* o, const float* lse, const __nv_bfloat16* d_o,
-                  float* delta, float* lse2, cudaStream_t s) {
+void launch_delta(const DevJobs& j, const __nv_bfloat16* o, const float* lse, const __nv_bfloat16* d_o_src,
+                  int64_t src_stride, __nv_bfloat16* d_o, float* delta, float* lse2, cudaStream_t s) {
   if (j.n_blocks)
     delta_kernel<<<j.n_blocks, 256, 0, s>>>(static_cast<const RowJob*>(j.jobs), j.job_of_block, j.first_chunk, o,
-                                            lse, d_o, delta, lse2);
+                                            lse, d_o_src, src_stride, d_o, delta, lse2);
 }
 void launch_return_accum(const DevJobs& j, cudaStream_t s) {
   if (j.n_blocks)

@@ -24,7 +24,7 @@ struct RowCopyJob {
 // Generic row job over 128-wide rows: a_row0 / b_row0 index rows of two arenas.
 struct RowJob {
   int64_t a_row0, b_row0;
-  int64_t b_stride;  // f32_to_bf16 only: b_row0 is an element offset, rows b_stride apart
+  int64_t b_stride;  // f32_to_bf16: b_row0 is an element offset, rows b_stride apart; delta: dO offset
   int32_t rows, _pad;
 };
 
@@ -42,8 +42,10 @@ void preload_movers();  // per current device, before any launch that others spi
 void launch_counter_add(uint32_t* c, cudaStream_t s);
 void launch_counter_wait(const uint32_t* c, const uint32_t* target, int n, cudaStream_t s);
 void launch_merge(const DevJobs& j, const int32_t* src_rows, __nv_bfloat16* o, float* lse, cudaStream_t s);
-void launch_delta(const DevJobs& j, const __nv_bfloat16* o, const float* lse, const __nv_bfloat16* d_o,
-                  float* delta, float* lse2, cudaStream_t s);
+// Delta / LSE2 preprocess fused with the dO scatter (d_o_src: the caller's packed dO,
+// src_stride elements between token rows; RowJob::b_stride = element offset of a job's row 0)
+void launch_delta(const DevJobs& j, const __nv_bfloat16* o, const float* lse, const __nv_bfloat16* d_o_src,
+                  int64_t src_stride, __nv_bfloat16* d_o, float* delta, float* lse2, cudaStream_t s);
 // jobs: RowCopyJob with src/dst = fp32 accumulators, rows of 128 floats (row_bytes ignored)
 void launch_return_accum(const DevJobs& j, cudaStream_t s);
 void launch_accum(const DevJobs& j, const __nv_bfloat16* src, float* dst, cudaStream_t s);

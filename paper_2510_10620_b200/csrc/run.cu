@@ -385,6 +385,8 @@ void Executor::backward(const void* const* d_o, void* const* dq, void* const* dk
   std::vector<char*> ddq(static_cast<size_t>(R_)), ddk(static_cast<size_t>(R_)), ddv(static_cast<size_t>(R_));
   for (int d = 0; d < R_; ++d) {
     ddo[d] = static_cast<const char*>(d_o[d]);
+    if (!host && local(d) && (reinterpret_cast<uintptr_t>(ddo[d]) & 15))  // (16-byte row loads)
+      throw Failure(DCPX_ERROR, "dcpx_backward: dO must be 16-byte aligned");
     ddq[d] = static_cast<char*>(dq ? dq[d] : nullptr);
     ddk[d] = static_cast<char*>(dk ? dk[d] : nullptr);
     ddv[d] = static_cast<char*>(dv ? dv[d] : nullptr);
@@ -439,9 +441,9 @@ void Executor::backward(const void* const* d_o, void* const* dq, void* const* dk
     // (overlapping the next forward; zero at prepare for the first call)
     CUDA_OK(cudaStreamWaitEvent(D.cs, D.aux_done, 0));
     if (acc_dirty_) zero_accumulators(d, D.cs);  // (the previous backward left them)
-    launch_row_copy(D.scatter_do.dj, D.cs, reinterpret_cast<int64_t>(ddo[d]), 0);
-    launch_delta(D.prep.dj, D.o, D.lse, D.d_o, D.delta, D.lse2, D.cs);
-    D.launches += 2;
+    launch_delta(D.prep.dj, D.o, D.lse, reinterpret_cast<const __nv_bfloat16*>(ddo[d]), g_.H * 128, D.d_o, D.delta,
+                 D.lse2, D.cs);
+    ++D.launches;
   }
   // every device's accumulators are zeroed before any peer returns into them: a device's
   // first gradient return waits for its peers' zeroing (not its attention)
