@@ -303,10 +303,32 @@ cudaEvent_t Executor::event(int d) {
 // transfer kernels on the (high-priority) comm stream run concurrently with compute.
 // Default 4 (profiles/r1_sm_reserve_sweep.log, cfg2 per-rank): N = 4 2910 vs 2817 TFLOP/s
 // with 8, N = 2 1624-1653 vs 1601-1609; one cfg3 N = 4 sample was 2 % slower (2482 vs 2531).
-int Executor::attn_grid(int d, int grid) const {
-  const int reserve = opt.sm_reserve >= 0 ? opt.sm_reserve : (R_ > 1 ? 4 : 0);
+// By default only launches that a fetch overlaps keep them (`overlap`, mark_fetch_overlap):
+// e.g. the last division's, which runs after every fetch has landed, takes all SMs.
+int Executor::attn_grid(int d, int grid, bool overlap) const {
+  const int reserve = opt.sm_reserve >= 0 ? opt.sm_reserve : (R_ > 1 && overlap ? 4 : 0);
   const int cap = std::max(1, num_sms(dev_[d].ordinal) - reserve);
   return std::min(grid, cap);
+}
+
+void Executor::mark_fetch_overlap(int d) {
+  auto& prog = dev_[d].prog;
+  const int T = plans_[d].divisions;
+  for (size_t i = 0; i < prog.size(); ++i) {
+    Op& op = prog[i];
+    if (op.kind != OpKind::kFwdAttn) continue;
+    bool f = false, b = false;
+    for (size_t k = i + 1; k < prog.size(); ++k) {
+      const Op& x = prog[k];
+      if (x.kind == OpKind::kFwdAttn && (x.num_units > 0 || x.bnum_units > 0)) break;
+      if (x.kind == OpKind::kCommWait && x.division < T) {
+        f |= x.jobs.dj.n_blocks > 0 || !x.xfer.empty();
+        b |= x.bjobs.dj.n_blocks > 0 || !x.bxfer.empty();
+      }
+    }
+    op.fetch_overlap = f;
+    op.bfetch_overlap = b;
+  }
 }
 
 // LOCAL transport on the DMA copy engines (option sm_transfers = 0), issued on the receiver's
@@ -635,6 +657,7 @@ void Executor::prepare(int nplans, const dcpx_plan_view* plans, const dcpx_graph
   build_transfer_jobs();
   for (int d = 0; d < R_; ++d) build_io_jobs(d);
   build_bwd_jobs();
+  for (int d = 0; d < R_; ++d) mark_fetch_overlap(d);
   for (int d = 0; d < R_; ++d) {
     DeviceGuard g(dev_[d].ordinal);
     CUDA_OK(cudaDeviceSynchronize());

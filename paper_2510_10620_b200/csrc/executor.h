@@ -95,6 +95,9 @@ struct Op {
   // persistent forward, receive side: the transfer overwrites slots once the units of
   // divisions < pf_wait_divs are done (the attention ops before its launch in program order)
   int pf_wait_divs = 0;
+  // attention: a fetch (CommWait of a division < T) follows before the next attention op in
+  // program order, i.e. runs on the comm stream while this launch does (forward / backward)
+  bool fetch_overlap = true, bfetch_overlap = true;
   std::string tag;
   std::vector<dcpx_block_slot> blocks;
   uint64_t bytes = 0;
@@ -255,7 +258,8 @@ class Executor {
   std::vector<std::array<double, 7>> trace_;
   void trace_begin();
   void copy_engine(const std::vector<RowCopyJob>& jobs, cudaStream_t s);
-  int attn_grid(int d, int grid) const;
+  int attn_grid(int d, int grid, bool overlap = true) const;
+  void mark_fetch_overlap(int d);
   void trace_collect();
   void compile_device(int d);
   void compile_attention(int d, int ins_index, std::vector<bool>& fused_red);

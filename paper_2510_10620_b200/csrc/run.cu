@@ -164,7 +164,7 @@ void Executor::forward(void* const* o_out, float* const* lse_out, dcpx_report* r
           p.epoch = epoch_;
         }
         std::pair<cudaEvent_t, cudaEvent_t> ke{};
-        const int grid = attn_grid(d, pers ? D.pf_grid : op.grid);
+        const int grid = pers ? attn_grid(d, D.pf_grid) : attn_grid(d, op.grid, op.fetch_overlap);
         p.sched = D.sched_ctr;
         p.sched_base = D.sched_base;
         D.sched_base += static_cast<uint32_t>(p.num_units + grid);
@@ -495,7 +495,7 @@ void Executor::backward(const void* const* d_o, void* const* dq, void* const* dk
           p.scale_log2 = static_cast<float>(1.4426950408889634) * scale;
           p.scale = scale;
           std::pair<cudaEvent_t, cudaEvent_t> ke{};
-          const int grid = attn_grid(d, op.bgrid);
+          const int grid = attn_grid(d, op.bgrid, op.bfetch_overlap);
           p.sched = D.sched_ctr;
           p.sched_base = D.sched_base;
           D.sched_base += static_cast<uint32_t>(op.bnum_units + grid);
