@@ -225,7 +225,8 @@ dcpx_status dcpx_load_inputs_host(dcpx_ctx* ctx, const void* q, const void* k, c
 dcpx_status dcpx_forward(dcpx_ctx* ctx, void* o_out, float* lse_out, dcpx_report* rep);
 dcpx_status dcpx_forward_host(dcpx_ctx* ctx, void* o_out, float* lse_out, dcpx_report* rep);
 
-/* Executes the backward of the last forward. d_o [T][H][D] bf16 in; dq [T][H][D],
+/* Executes the backward of the last forward. d_o [T][H][D] bf16 in (device memory, 16-byte
+ * aligned: rows are read as 16-byte vectors; DCPX_ERROR otherwise); dq [T][H][D],
  * dk, dv [T][G][D] bf16 out (owned rows). */
 dcpx_status dcpx_backward(dcpx_ctx* ctx, const void* d_o, void* dq, void* dk, void* dv,
                           dcpx_report* rep);
