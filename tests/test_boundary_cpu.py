@@ -206,3 +206,18 @@ def test_item_sample_bundle_and_reference_items():
         fin = l2 > 0
         assert np.array_equal(np.isfinite(l), fin)
         assert np.abs(l[fin] - (m2[fin] + np.log(l2[fin]))).max() <= 1e-12
+
+
+def test_package_import_sets_hardware_queue_count():
+    """Importing the package before any CUDA call defaults CUDA_DEVICE_MAX_CONNECTIONS to 32
+    (the compute and comm streams must not share a hardware work queue,
+    profiles/r2_n4_scheduler_queues_persistent.md); a caller's own setting wins."""
+    import subprocess
+    import sys
+    code = "import os, paper_2510_10620_b200; print(os.environ.get('CUDA_DEVICE_MAX_CONNECTIONS'))"
+    env = {k: v for k, v in os.environ.items() if k != "CUDA_DEVICE_MAX_CONNECTIONS"}
+    out = subprocess.run([sys.executable, "-c", code], env=env, cwd=REPO, capture_output=True, text=True)
+    assert out.stdout.strip() == "32", out.stderr
+    env["CUDA_DEVICE_MAX_CONNECTIONS"] = "16"
+    out = subprocess.run([sys.executable, "-c", code], env=env, cwd=REPO, capture_output=True, text=True)
+    assert out.stdout.strip() == "16", out.stderr
