@@ -27,6 +27,13 @@
 #include "program.h"
 #include "sm100.cuh"
 
+// The forward's scheduler ring holds one unit: its TMA warp needs no more look-ahead, and
+// claiming later keeps short launches balanced (fwd kernel -0.6 % cfg3 N = 1, -5 % cfg2
+// N = 4 vs depth 2; profiles/r2_n4_scheduler_queues_persistent.md section 7).
+#ifndef DCPX_FWD_SCHED_RING
+#define DCPX_FWD_SCHED_RING 1
+#endif
+
 namespace dcpx {
 
 // Column pairs (of every 16) whose exp2 is evaluated by soft_exp2 instead of MUFU.
@@ -74,7 +81,7 @@ struct FwdBarriers {
   uint64_t q_full, q_empty;
   uint64_t k_full[2], v_full[2], kv_empty[2];
   uint64_t s_full[2], p_half[2], p_ready[2], o_full[2], o_empty[2];
-  SchedRing sched;  // unit indices from the dynamic scheduler (warp 2)
+  SchedRingN<DCPX_FWD_SCHED_RING> sched;  // unit indices from the dynamic scheduler (warp 2)
   uint32_t tmem_base;
 };
 

@@ -223,27 +223,34 @@ __device__ __forceinline__ void wait_stamp(const uint32_t* p, uint32_t v) {
 // The counter is never reset: every launch advances it by exactly num_units + gridDim.x
 // (each CTA's scheduler stops after its first fetch past the end), so the host passes the
 // launch's base value and keeps the running sum (modulo 2^32).
+// Ring depth = how many units a CTA may claim ahead of its slowest role: 2 lets the TMA
+// warp run two units ahead without one CTA hoarding a short launch's units
+// (profiles/r2_n4_scheduler_queues_persistent.md); the forward kernel may use its own depth.
 #ifndef DCPX_SCHED_RING
 #define DCPX_SCHED_RING 2
 #endif
 constexpr int kSchedRing = DCPX_SCHED_RING;
-struct SchedRing {
-  uint64_t full[kSchedRing], empty[kSchedRing];
-  int32_t unit[kSchedRing];
+template <int N>
+struct SchedRingN {
+  uint64_t full[N], empty[N];
+  int32_t unit[N];
 };
+using SchedRing = SchedRingN<kSchedRing>;
 
-__device__ __forceinline__ void sched_init(SchedRing& r, uint32_t consumer_warps) {
-  for (int i = 0; i < kSchedRing; ++i) {
+template <int N>
+__device__ __forceinline__ void sched_init(SchedRingN<N>& r, uint32_t consumer_warps) {
+  for (int i = 0; i < N; ++i) {
     mbar_init(&r.full[i], 1);
     mbar_init(&r.empty[i], consumer_warps);
   }
 }
 
 // Scheduler side (one thread). Writes -1 once the units are exhausted and returns.
-__device__ __forceinline__ void sched_produce(SchedRing& r, uint32_t* ctr, uint32_t base, int num_units) {
+template <int N>
+__device__ __forceinline__ void sched_produce(SchedRingN<N>& r, uint32_t* ctr, uint32_t base, int num_units) {
   for (uint32_t k = 0;; ++k) {
-    const uint32_t s = k % kSchedRing;
-    mbar_wait(&r.empty[s], ((k / kSchedRing) & 1) ^ 1);
+    const uint32_t s = k % N;
+    mbar_wait(&r.empty[s], ((k / N) & 1) ^ 1);
     const uint32_t t = atomicAdd(ctr, 1u) - base;
     const int u = t < static_cast<uint32_t>(num_units) ? static_cast<int>(t) : -1;
     *reinterpret_cast<volatile int32_t*>(&r.unit[s]) = u;
@@ -253,9 +260,10 @@ __device__ __forceinline__ void sched_produce(SchedRing& r, uint32_t* ctr, uint3
 }
 
 // Consumer side (a converged warp): the next unit of this CTA, or -1 at the end.
-__device__ __forceinline__ int sched_next(SchedRing& r, uint32_t& k) {
-  const uint32_t s = k % kSchedRing;
-  mbar_wait(&r.full[s], (k / kSchedRing) & 1);
+template <int N>
+__device__ __forceinline__ int sched_next(SchedRingN<N>& r, uint32_t& k) {
+  const uint32_t s = k % N;
+  mbar_wait(&r.full[s], (k / N) & 1);
   const int u = *reinterpret_cast<volatile int32_t*>(&r.unit[s]);
   jitter_point();
   __syncwarp();
