@@ -188,6 +188,7 @@ __device__ __forceinline__ void red_release_gpu_add(uint32_t* p, uint32_t v) {
 // surfaces as a launch error. Then orders the generic-proxy acquire before later async-proxy
 // (TMA) reads of the data the signal published.
 __device__ __forceinline__ void wait_counter(const uint32_t* p, uint32_t target) {
+  jitter_point();  // (race-detection build: late pollers)
   if (ld_acquire_gpu(p) < target) {
     const uint64_t t0 = global_ns();
     while (ld_acquire_gpu(p) < target) {
@@ -205,6 +206,7 @@ __device__ __forceinline__ void wait_counter(const uint32_t* p, uint32_t target)
 }
 // Spins until *p == v (an epoch stamp), acquire.
 __device__ __forceinline__ void wait_stamp(const uint32_t* p, uint32_t v) {
+  jitter_point();
   if (ld_acquire_gpu(p) == v) return;
   const uint64_t t0 = global_ns();
   while (ld_acquire_gpu(p) != v) {

@@ -72,3 +72,19 @@ def test_jitter_build_per_rank_flags(R, tmp_path):
                 assert np.array_equal(got, want[key].astype(np.float64)), (tag, key)
             else:
                 assert rel_err(got, want[key]) <= 4e-3, (tag, key)
+
+
+def test_jitter_build_persistent_forward():
+    """The persistent forward's device-side ordering (fetch counter, per-tile unit stamps,
+    slot-free counters) under late pollers: tests/test_gpu_persistent.py run against the
+    jitter build, i.e. (O, LSE) of the persistent launch bit-identical to the per-division
+    launches with every wait perturbed. Needs one GPU per plan device."""
+    import torch
+    if torch.cuda.device_count() < 2:
+        pytest.skip("the persistent forward needs one GPU per plan device")
+    assert os.path.exists(JITTER), "jitter build missing (tools/build.py builds it)"
+    env = dict(os.environ, DCPX_LIB=JITTER)
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-m", "gpu",
+                        os.path.join(REPO, "tests", "test_gpu_persistent.py")],
+                       capture_output=True, text=True, timeout=900, env=env, cwd=REPO)
+    assert r.returncode == 0 and " passed" in r.stdout, r.stdout[-3000:] + r.stderr[-3000:]
