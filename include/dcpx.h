@@ -277,7 +277,9 @@ dcpx_status dcpx_debug_arena(dcpx_ctx* ctx, int dev, int kind, void** ptr, int64
 /* Executor options: "fuse_reductions", "remap_copies", "timing" (report device_ms; blocks
  * the host at the end of each call; default off), "kernel_timing" (1: per-call attention
  * kernel times in the report, blocking; 2: deferred, see dcpx_kernel_times), "trace", "sm_transfers",
- * "sm_reserve", "bwd_order", "bwd_window", "bwd_window_min_steps", "bwd_merge_heads",
+ * "sm_reserve" (SMs an attention launch leaves to the comm stream's copy kernels; default -1:
+ * 4 on launches a fetch overlaps in multi-device plans, 0 otherwise; >= 0: that many on every
+ * launch), "bwd_order", "bwd_window", "bwd_window_min_steps", "bwd_merge_heads",
  * "persistent" (1: one forward launch per device for all divisions, ordered on the device;
  * default 0), "aux_zero" (1, default: the gradient accumulators are re-zeroed on an aux
  * stream after each backward; 0: at the start of the next one).
